@@ -1,0 +1,325 @@
+#!/usr/bin/env python
+"""Benchmark: full-Greeks Heston Milstein Monte Carlo on B200.
+
+Headline workload (BASELINE.json configs[2], the metric's own config):
+arithmetic-Asian call, 252 daily fixings, 2^24 paths x 252 Milstein steps,
+BASELINE parameter set A, price + Delta + Gamma + Vega + Rho (+ FD Delta,
+FD Rho) from ONE fused pass with common-random-number bumps.  A bench
+"step" is one complete full-Greeks evaluation of that job.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+N > 1: launched under torch.distributed.run, one rank per GPU over NCCL; the
+2^24 paths are split across ranks (strong scaling) and the chunk partials
+are all-gathered once per step.  Rank 0 prints ONE JSON line.
+
+--impl reference: the reference's own compiled CPU kernel (oracle/_ref,
+built from the reference's _core.c) driven by the restated reference engine
+on all host cores, on a bounded sample of the same workload (rank 0 only).
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_PATHS = 2 ** 24
+N_STEPS = 252
+METRIC = "path_steps_per_sec_full_greeks"
+UNIT = "path-steps/s"
+MUFU_PER_PATH_STEP = 10      # BASELINE.md roofline: Asian full Greeks
+FP32_PER_PATH_STEP = 45
+N_SM = 148
+
+
+def workload():
+    from paper_2309_10477_b200 import BENCH_PARAMS, HestonParams, OptionSpec, SimConfig, daily_fixings
+    p = HestonParams(**BENCH_PARAMS)
+    spec = OptionSpec("asian_arithmetic", "call", 100.0, 1.0, 100.0,
+                      averaging_times=daily_fixings(1.0, N_STEPS))
+    cfg = SimConfig(scheme="milstein", sampler="pseudo", n_paths=N_PATHS, n_steps=N_STEPS,
+                    n_runs=1, seed=42, precision="fp32")
+    return p, spec, cfg
+
+
+def config_block(n_gpus: int) -> dict:
+    return {"workload": "asian_arith_call_daily_fixings_full_greeks",
+            "paths": N_PATHS, "time_steps": N_STEPS, "fixings": N_STEPS, "scheme": "milstein",
+            "greeks": ["price", "delta", "gamma", "vega", "rho", "delta_fd", "rho_fd"],
+            "params": "BASELINE A: S0=K=100 T=1 r=0.03 v0=0.04 kappa=2 theta=0.04 xi=0.3 rho=-0.7",
+            "rng": "philox4x32-10 + box-muller", "state": "fp32 registers", "sums": "fp64",
+            "l2": "256 MiB buffer written between timed iterations (kernel has no HBM inputs)",
+            "parallelism": f"dp{n_gpus}"}
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (NVML)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001 - clocks are reported as unavailable
+            self.nv = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.nv:
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle/_ref = the reference's own compiled kernel)
+# ---------------------------------------------------------------------------
+def cpu_reference_pass(n_paths: int, workers: int) -> float:
+    """Full-Greeks set the reference way: engine.greeks (price, pathwise
+    Delta/Rho) + 4 CRN re-runs with S0 +/- h and v0 +/- h for Gamma/Vega
+    (BASELINE.md CPU-baseline plan).  Returns wall seconds."""
+    from oracle import engine as oe
+    from paper_2309_10477_b200 import HestonParams, OptionSpec, SimConfig
+    p, spec, _ = workload()
+    cfg = SimConfig(scheme="milstein", n_paths=n_paths, n_steps=N_STEPS, n_runs=1, seed=42)
+    h = 0.005 * spec.spot
+    hv = 0.01 * p.v0
+    bump_s = lambda d: OptionSpec(spec.style, spec.right, spec.strike, spec.maturity,  # noqa: E731
+                                  spec.spot + d, spec.averaging_times)
+    bump_v = lambda d: HestonParams(p.kappa, p.theta, p.sigma, p.rho, p.r, p.v0 + d)  # noqa: E731
+    t0 = time.perf_counter()
+    oe.per_run_values(p, spec, cfg, True, "reference", workers)
+    for s in (bump_s(h), bump_s(-h)):
+        oe.per_run_values(p, s, cfg, False, "reference", workers)
+    for pp in (bump_v(hv), bump_v(-hv)):
+        oe.per_run_values(pp, spec, cfg, False, "reference", workers)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline_block(n_paths: int = 2 ** 16) -> dict:
+    import oracle
+    workers = os.cpu_count() or 1
+    kind = "reference" if oracle.ref_core() is not None else "port"
+    if kind == "port":
+        return {"value": None, "unit": UNIT, "cores": workers, "kind": "port",
+                "sample": "oracle/_ref missing; not timed"}
+    cpu_reference_pass(2 ** 12, workers)  # warm the pool / page in
+    secs = cpu_reference_pass(n_paths, workers)
+    return {"value": n_paths * N_STEPS / secs, "unit": UNIT, "cores": workers, "kind": kind,
+            "sample": f"{n_paths} paths x {N_STEPS} steps, Asian daily fixings, full Greeks as "
+                      f"greeks() + 4 CRN bumped price() passes, {secs:.2f} s wall",
+            "seconds": secs}
+
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    workers = os.cpu_count() or 1
+    if oracle.ref_core() is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    n = 2 ** 15
+    for _ in range(args.warmup):
+        cpu_reference_pass(n, workers)
+    times = [cpu_reference_pass(n, workers) for _ in range(args.steps)]
+    secs = sum(times) / len(times)
+    value = n * N_STEPS / secs
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1000.0,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference", "config": config_block(args.gpus),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "reference",
+                             "sample": f"{n} of the {N_PATHS} paths per step (bounded sample), "
+                                       "reference _core kernel + restated reference engine, "
+                                       "full Greeks = greeks() + 4 CRN bumped price() passes"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+def run_b200(args) -> None:
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2309_10477_b200 import _lib, engine, greeks, parallel
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    p, spec, cfg = workload()
+    L = _lib.lib()
+
+    # resident job: structs, workspace and partial buffers allocated once
+    job = engine.Job(p, spec, cfg, True)
+    sl = parallel.shard(cfg.n_paths, rank, world)
+    job.sim.path_lo, job.sim.path_hi = sl.path_lo, sl.path_hi
+    stream = torch.cuda.current_stream(dev)
+    work = torch.empty(int(L.hmc_workspace_bytes(ctypes.byref(job.sim))), dtype=torch.uint8, device=dev)
+    loc = torch.zeros((cfg.n_runs, sl.n_chunks, _lib.HMC_NW), dtype=torch.float64, device=dev)
+    out = torch.empty((cfg.n_runs, _lib.HMC_NW), dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
+    launches_per_step = 3  # path kernel + tiles->chunks + chunks->runs
+
+    def step(ev0=None, ev1=None):
+        if ev0 is not None:
+            ev0.record(stream)
+        _lib.check(L.hmc_greeks_chunks(ctypes.byref(job.model), ctypes.byref(job.product),
+                                       ctypes.byref(job.sim), ctypes.c_void_p(loc.data_ptr()),
+                                       ctypes.c_void_p(work.data_ptr()),
+                                       ctypes.c_void_p(stream.cuda_stream)))
+        if ev1 is not None:
+            ev1.record(stream)
+        full = parallel.gather_chunks(loc, cfg.n_paths)
+        _lib.check(L.hmc_reduce_chunks(ctypes.c_void_p(full.data_ptr()), cfg.n_runs, full.shape[1],
+                                       ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(stream.cuda_stream)))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for e0, e1, e2 in ev:
+            flush.fill_(1)                       # evict L2 between timed iterations
+            step(e0, e1)
+            e2.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [e0.elapsed_time(e2) for e0, _, e2 in ev]
+    kern_ms = [e0.elapsed_time(e1) for e0, e1, _ in ev]
+    t = torch.tensor([sum(step_ms), sum(kern_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t[0]) / args.steps
+    kernel_ms = float(t[1]) / args.steps
+    path_steps = cfg.n_paths * N_STEPS
+    value = path_steps / (ms_per_step / 1000.0)
+    res_dev = out.cpu().numpy()
+
+    # e2e: the public API call a user makes (host structs in, host McSummary
+    # out; step tables H2D and sums D2H inside every timed call)
+    e2e_times = []
+    g = None
+    for i in range(max(2, args.steps // 2) + 1):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        g = greeks(p, spec, cfg)
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_s = sorted(e2e_times[1:])[len(e2e_times[1:]) // 2]
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_s = float(te[0])
+    h2d = (N_STEPS + 1) * (32 + 16) + job.avg_idx.nbytes
+    d2h = cfg.n_runs * _lib.HMC_NW * 8
+
+    if rank == 0:
+        clk = clocks.summary()
+        f_mhz = clk["sm_mhz"] or 1965.0
+        peak = N_SM * 16 * f_mhz * 1e6 / MUFU_PER_PATH_STEP  # per GPU
+        local_path_steps = sl.n_paths * N_STEPS
+        achieved = local_path_steps / (kernel_ms / 1000.0)
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": config_block(world),
+            "full_greeks_wall_ms": ms_per_step,
+            "kernel_ms": kernel_ms,
+            "roofline": {"bound": "mufu", "achieved": achieved, "peak": peak, "unit": UNIT,
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": f"{N_SM} SM x 16 MUFU/clk x {f_mhz:.0f} MHz (sampled) / "
+                                        f"{MUFU_PER_PATH_STEP} MUFU per path-step (BASELINE.md)",
+                         "fp32_peak": N_SM * 128 * f_mhz * 1e6 / FP32_PER_PATH_STEP},
+            "e2e": {"value": path_steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_call": e2e_s * 1000.0},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk,
+            "estimates": {q: [g[q].estimate, g[q].path_std_error] for q in g},
+        }
+        if world == 1 and not args.no_cpu:
+            line["cpu_baseline"] = cpu_baseline_block()
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

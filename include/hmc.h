@@ -1,0 +1,172 @@
+/*
+ * hmc.h -- C ABI of libhmc.so, the B200 (sm_100a) Heston Monte Carlo Greeks
+ * engine.  Plain C types only: no torch, no C++ in the signatures.
+ *
+ * Reference interfaces each entry point replaces (reference =
+ * /root/reference/pkg/src/hestonmc):
+ *
+ *   hmc_discretised_batch_f64  <- backend module call
+ *                                 discretised_batch(params, s0, T, n_steps,
+ *                                 milstein, path_lo, path_hi, key_run,
+ *                                 uniforms, avg_indices)
+ *                                 _core.pyx:354-412, _batch_py.py:36-81,
+ *                                 called from engine.py:87-90
+ *   hmc_greeks / hmc_greeks_chunks + hmc_reduce_chunks
+ *                              <- engine._run_sums + _simulate_chunk +
+ *                                 _per_path_stats (engine.py:47-116): one
+ *                                 fused pass over all runs x paths producing
+ *                                 per-run sums and sums of squares of
+ *                                 price / Delta / Rho (+ Gamma, Vega, FD
+ *                                 Delta, FD Rho from CRN bumps)
+ *   hmc_sobol_init_directions  <- scipy.stats.qmc.Sobol direction numbers
+ *                                 used by rng.sobol_points (rng.py:143-152)
+ *   hmc_root_key / hmc_derive_key
+ *                              <- rng.root_key / rng.derive_key (rng.py:46-52)
+ *
+ * Errors: every function returns 0 on success or a negative HMC_E* code;
+ * hmc_last_error() gives a thread-local message for the last failure.
+ * Threading: all entry points are re-entrant (no global mutable state apart
+ * from the thread-local error string); buffers are caller-owned.
+ */
+#ifndef HMC_H_
+#define HMC_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HMC_ABI_VERSION 1
+
+/* reduction geometry -- fixed so results never depend on grid size or GPU count */
+#define HMC_TILE 128          /* paths per thread block == per tile partial   */
+#define HMC_CHUNK_TILES 128   /* tiles per chunk partial                      */
+#define HMC_CHUNK (HMC_TILE * HMC_CHUNK_TILES) /* 16384 paths per chunk      */
+#define HMC_NQ 7              /* per-path quantities, order below             */
+#define HMC_NW (2 * HMC_NQ)   /* {sum, sum of squares} per quantity           */
+
+/* quantity index q: partial[2*q] = sum_x, partial[2*q+1] = sum_x^2 */
+enum {
+    HMC_Q_PRICE = 0,    /* discounted payoff                engine.py:53-56 */
+    HMC_Q_DELTA = 1,    /* pathwise Delta                   engine.py:58-59 */
+    HMC_Q_RHO = 2,      /* pathwise Rho                     engine.py:60-67 */
+    HMC_Q_GAMMA = 3,    /* CRN FD of pathwise Delta, S0+-h     */
+    HMC_Q_VEGA = 4,     /* CRN FD of price in v0            (north star)    */
+    HMC_Q_DELTA_FD = 5, /* CRN FD of price in S0     test_products.py:101   */
+    HMC_Q_RHO_FD = 6    /* CRN FD of price in r      test_products.py:114   */
+};
+
+enum {
+    HMC_OK = 0,
+    HMC_E_INVALID = -1,   /* bad argument            -> ValidationError     */
+    HMC_E_CUDA = -2,      /* CUDA runtime failure    -> DeviceError         */
+    HMC_E_NODEVICE = -3,  /* no CUDA device visible  -> DeviceError         */
+    HMC_E_UNSUPPORTED = -4 /* e.g. Greeks for a put  -> UnsupportedProduct  */
+};
+
+enum { HMC_STYLE_EUROPEAN = 0, HMC_STYLE_ASIAN = 1 };
+enum { HMC_CALL = 0, HMC_PUT = 1 };
+enum { HMC_SCHEME_EULER = 1, HMC_SCHEME_MILSTEIN = 2 };
+enum { HMC_SAMPLER_PSEUDO = 0, HMC_SAMPLER_SOBOL = 1 };
+enum {
+    HMC_PREC_FP32 = 0, /* Philox4x32-10 / Sobol, fp32 state, fp64 sums      */
+    HMC_PREC_FP64 = 1  /* reference SplitMix64 / Sobol + Acklam-Halley ndtri,
+                          fp64 state, the reference's operation order        */
+};
+
+/* HestonParams (model.py:11-45) */
+typedef struct hmc_model {
+    double kappa, theta, sigma, rho, r, v0;
+} hmc_model;
+
+/* OptionSpec (model.py:54-87) + averaging grid indices (engine.py:81-86) */
+typedef struct hmc_product {
+    int32_t style;          /* HMC_STYLE_*                                   */
+    int32_t right;          /* HMC_CALL / HMC_PUT                            */
+    double strike, maturity, spot;
+    const int64_t* avg_idx; /* HOST pointer, strictly increasing in 1..n_steps;
+                               european: {n_steps}                           */
+    int64_t n_avg;
+} hmc_product;
+
+/* SimConfig (model.py:140-180) + this call's slice of the path axis */
+typedef struct hmc_sim {
+    int32_t scheme;       /* HMC_SCHEME_*                                    */
+    int32_t sampler;      /* HMC_SAMPLER_*                                   */
+    int32_t precision;    /* HMC_PREC_*                                      */
+    int32_t want_greeks;  /* 0: price column only                            */
+    int32_t n_steps;
+    int32_t n_runs;
+    int64_t n_paths;      /* paths per run (whole job)                       */
+    int64_t path_lo;      /* this slice: [path_lo, path_hi), path_lo % HMC_CHUNK == 0 */
+    int64_t path_hi;
+    uint64_t seed;
+    double h_spot;        /* absolute S0 bump                                */
+    double v0_up, v0_dn;  /* start variances of the two v0-bumped trajectories */
+    double h_r;           /* absolute r bump                                 */
+    const uint32_t* sobol_v; /* sobol only: [30][2*n_steps] direction numbers
+                                (hmc_sobol_init_directions layout)           */
+    int32_t sobol_v_on_device; /* 1: sobol_v is a device pointer of the
+                                  current device; 0: host pointer            */
+    int32_t reserved;
+} hmc_sim;
+
+int hmc_abi_version(void);
+const char* hmc_last_error(void);
+int hmc_device_count(int32_t* count);
+
+/* number of chunk partials this slice produces per run */
+int64_t hmc_chunks_in_slice(const hmc_sim* sim);
+/* device workspace bytes hmc_greeks_chunks needs for this slice */
+int64_t hmc_workspace_bytes(const hmc_sim* sim);
+
+/* Launch the fused path + Greeks kernel for [path_lo, path_hi) x all runs on
+ * `stream` (cudaStream_t, NULL = legacy default) of the CURRENT device and
+ * write chunk partials d_chunks[run][chunk][HMC_NW] (device, fp64).
+ * d_work: device scratch of hmc_workspace_bytes(sim) bytes.  Asynchronous. */
+int hmc_greeks_chunks(const hmc_model* model, const hmc_product* product,
+                      const hmc_sim* sim, double* d_chunks, void* d_work,
+                      void* stream);
+
+/* Fixed-order (compensated, sequential) sum of chunk partials
+ * d_chunks[run][0..n_chunks)[HMC_NW] -> d_out[run][HMC_NW].  Chunks must be
+ * in global path order; the result is then bit-identical for any split of
+ * the path axis across calls / GPUs.  Asynchronous on `stream`. */
+int hmc_reduce_chunks(const double* d_chunks, int32_t n_runs, int64_t n_chunks,
+                      double* d_out, void* stream);
+
+/* Convenience: whole job on one device, synchronous, HOST output
+ * h_out[run][HMC_NW].  Inputs are host structs; sim->path_lo/hi are ignored
+ * (the full [0, n_paths) range is simulated). */
+int hmc_greeks(const hmc_model* model, const hmc_product* product,
+               const hmc_sim* sim, double* h_out, int32_t device);
+
+/* Reference backend call discretised_batch (_core.pyx:354-412) in fp64 on
+ * the GPU: same key derivation, draw layout and arithmetic order.
+ * uniforms: HOST (path_hi-path_lo, 2*n_steps) row-major or NULL (in-kernel
+ * SplitMix64 stream); avg_idx: HOST; out: HOST (path_hi-path_lo, 3)
+ * [s_T, avg, tw_sum].  Synchronous. */
+int hmc_discretised_batch_f64(const hmc_model* model, double s0, double T,
+                              int32_t n_steps, int32_t milstein,
+                              int64_t path_lo, int64_t path_hi,
+                              uint64_t key_run, const double* uniforms,
+                              const int64_t* avg_idx, int64_t n_avg,
+                              double* out, int32_t device);
+
+/* Joe-Kuo direction numbers as used by scipy.stats.qmc.Sobol(scramble=False)
+ * (30 bits): poly[dim], vinit[dim][18] from scipy's
+ * _sobol_direction_numbers.npz -> v_out[30][dim] (HOST).  Point n of the
+ * Gray-code sequence is x_d(n) = 2^-30 * XOR_{b : bit b of n^(n>>1)} v[b][d]. */
+int hmc_sobol_init_directions(const int64_t* poly, const int64_t* vinit,
+                              int32_t dim, uint32_t* v_out);
+
+/* Key derivation of the reference RNG (rng.py:46-52), for hosts that
+ * build key_run for hmc_discretised_batch_f64. */
+uint64_t hmc_root_key(uint64_t seed);
+uint64_t hmc_derive_key(uint64_t parent, uint64_t index);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HMC_H_ */

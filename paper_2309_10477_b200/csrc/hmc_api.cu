@@ -1,0 +1,452 @@
+// hmc_api.cu -- the C ABI (include/hmc.h): argument validation, per-call
+// step tables, kernel dispatch, and the fixed-order reductions
+//   tile partials (128 paths)  ->  chunk partials (16384 paths)  ->  per run.
+// Chunks are the unit exchanged between GPUs, so a job split across any
+// number of devices at chunk boundaries reduces in exactly the single-GPU
+// order (bit-identical results, the reference's determinism contract,
+// engine.py:5-9).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "hmc_device.cuh"
+#include "hmc_launch.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define HMC_CK(expr)                                                                  \
+    do {                                                                              \
+        cudaError_t e_ = (expr);                                                      \
+        if (e_ != cudaSuccess)                                                        \
+            return fail(e_ == cudaErrorNoDevice || e_ == cudaErrorInsufficientDriver  \
+                            ? HMC_E_NODEVICE                                          \
+                            : HMC_E_CUDA,                                             \
+                        std::string(#expr) + ": " + cudaGetErrorString(e_));          \
+    } while (0)
+
+using hmc::KernelArgs;
+using hmc::StepD;
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+long long n_tiles_of(long long n) { return (n + HMC_TILE - 1) / HMC_TILE; }
+long long n_chunks_of(long long n) { return (n + HMC_CHUNK - 1) / HMC_CHUNK; }
+
+struct Prepared {
+    KernelArgs a{};
+    std::vector<StepD> st64;
+    std::vector<float4> st32;
+    long long n_tiles = 0, n_chunks = 0;
+    size_t off_st64 = 0, off_st32 = 0, off_sobol = 0, bytes = 0;
+};
+
+int check_model(const hmc_model* m) {
+    if (!m) return fail(HMC_E_INVALID, "model is NULL");
+    if (!(m->kappa > 0.0) || !(m->theta > 0.0) || !(m->sigma > 0.0))
+        return fail(HMC_E_INVALID, "kappa, theta and sigma must be > 0");
+    if (!(m->rho >= -1.0 && m->rho <= 1.0)) return fail(HMC_E_INVALID, "rho must lie in [-1, 1]");
+    if (!(m->v0 >= 0.0)) return fail(HMC_E_INVALID, "v0 must be >= 0");
+    return HMC_OK;
+}
+
+// step table shared by every kernel: t_k = k*T/n_steps computed exactly as
+// _core.pyx:406 (int k promoted to double, times T, divided by n_steps)
+void build_steps(int n_steps, double T, double h_r, const unsigned char* fix, Prepared& P) {
+    P.st64.resize((size_t)n_steps + 1);
+    P.st32.resize((size_t)n_steps + 1);
+    for (int k = 0; k <= n_steps; ++k) {
+        const double t = k * T / n_steps;
+        StepD s{t, std::expm1(h_r * t), std::expm1(-h_r * t), fix[k] ? 1.0 : 0.0};
+        P.st64[k] = s;
+        P.st32[k] = make_float4((float)s.t, (float)s.e1p, (float)s.e1m, (float)s.fix);
+    }
+}
+
+void fill_fp32_constants(KernelArgs& a) {
+    const double log2e = 1.4426950408889634074, ln2 = 0.69314718055994530942;
+    const double mil = a.milstein ? 1.0 : 0.0;
+    a.f_omkdt = (float)(1.0 - a.kappa * a.dt);
+    a.f_ck0 = (float)(a.kappa * a.theta * a.dt - mil * 0.25 * a.sigma * a.sigma * a.dt);
+    a.f_cmil = (float)(mil * 0.25 * a.sigma * a.sigma);
+    a.f_sigma = (float)a.sigma;
+    a.f_nhdt2 = (float)(-0.5 * a.dt * log2e);
+    a.f_bm = (float)(-2.0 * ln2 * a.dt);
+    a.f_rl2 = (float)(a.r * log2e);
+    a.f_l2s0 = (float)std::log2(a.s0);
+    a.f_log2e = (float)log2e;
+    a.f_rho = (float)a.rho;
+    a.f_sq1mr2 = (float)a.sq1mr2;
+    a.f_sqdt = (float)std::sqrt(a.dt);
+}
+
+int prepare(const hmc_model* m, const hmc_product* pr, const hmc_sim* sim, Prepared& P) {
+    int rc = check_model(m);
+    if (rc) return rc;
+    if (!pr || !sim) return fail(HMC_E_INVALID, "product/sim is NULL");
+    if (!(pr->strike > 0.0) || !(pr->maturity > 0.0) || !(pr->spot > 0.0))
+        return fail(HMC_E_INVALID, "strike, maturity and spot must be > 0");
+    if (pr->style != HMC_STYLE_EUROPEAN && pr->style != HMC_STYLE_ASIAN)
+        return fail(HMC_E_INVALID, "unknown option style");
+    if (pr->right != HMC_CALL && pr->right != HMC_PUT) return fail(HMC_E_INVALID, "unknown option right");
+    if (sim->scheme != HMC_SCHEME_EULER && sim->scheme != HMC_SCHEME_MILSTEIN)
+        return fail(HMC_E_UNSUPPORTED, "only the euler and milstein schemes run on the GPU");
+    if (sim->sampler != HMC_SAMPLER_PSEUDO && sim->sampler != HMC_SAMPLER_SOBOL)
+        return fail(HMC_E_INVALID, "unknown sampler");
+    if (sim->precision != HMC_PREC_FP32 && sim->precision != HMC_PREC_FP64)
+        return fail(HMC_E_INVALID, "unknown precision");
+    if (sim->n_steps < 1 || sim->n_runs < 1 || sim->n_runs > 65535 || sim->n_paths < 1)
+        return fail(HMC_E_INVALID, "need n_steps >= 1, 1 <= n_runs <= 65535, n_paths >= 1");
+    if (sim->path_lo < 0 || sim->path_hi > sim->n_paths || sim->path_lo >= sim->path_hi)
+        return fail(HMC_E_INVALID, "path slice must satisfy 0 <= path_lo < path_hi <= n_paths");
+    if (sim->path_lo % HMC_CHUNK != 0) return fail(HMC_E_INVALID, "path_lo must be a multiple of HMC_CHUNK");
+    if (sim->want_greeks && pr->right != HMC_CALL)
+        return fail(HMC_E_UNSUPPORTED, "pathwise Greeks are derived for calls only");
+    if (!pr->avg_idx || pr->n_avg < 1) return fail(HMC_E_INVALID, "avg_idx must hold >= 1 index");
+    for (long long i = 0; i < pr->n_avg; ++i) {
+        if (pr->avg_idx[i] < 1 || pr->avg_idx[i] > sim->n_steps ||
+            (i > 0 && pr->avg_idx[i] <= pr->avg_idx[i - 1]))
+            return fail(HMC_E_INVALID, "avg_idx must be strictly increasing in [1, n_steps]");
+    }
+    if (pr->style == HMC_STYLE_EUROPEAN && (pr->n_avg != 1 || pr->avg_idx[0] != sim->n_steps))
+        return fail(HMC_E_INVALID, "european products fix once, at n_steps");
+    if (sim->want_greeks) {
+        if (!(sim->h_spot > 0.0 && sim->h_spot < pr->spot)) return fail(HMC_E_INVALID, "need 0 < h_spot < spot");
+        if (!(sim->v0_up > sim->v0_dn && sim->v0_dn >= 0.0)) return fail(HMC_E_INVALID, "need v0_up > v0_dn >= 0");
+        if (!(sim->h_r > 0.0)) return fail(HMC_E_INVALID, "need h_r > 0");
+    }
+    if (sim->sampler == HMC_SAMPLER_SOBOL) {
+        if (!sim->sobol_v) return fail(HMC_E_INVALID, "sobol sampler needs direction numbers");
+        if (1.0 + (double)sim->n_runs * (double)sim->n_paths > 1073741824.0)
+            return fail(HMC_E_INVALID, "sobol index range exceeds 2^30 points");
+    }
+
+    KernelArgs& a = P.a;
+    a.kappa = m->kappa; a.theta = m->theta; a.sigma = m->sigma; a.rho = m->rho;
+    a.r = m->r; a.v0 = m->v0;
+    a.s0 = pr->spot; a.T = pr->maturity; a.K = pr->strike;
+    a.v0_up = sim->want_greeks ? sim->v0_up : m->v0;
+    a.v0_dn = sim->want_greeks ? sim->v0_dn : m->v0;
+    a.h_spot = sim->want_greeks ? sim->h_spot : 0.0;
+    a.h_r = sim->want_greeks ? sim->h_r : 0.0;
+    a.dt = pr->maturity / sim->n_steps;                    // _core.pyx:378
+    a.sq1mr2 = std::sqrt(1.0 - m->rho * m->rho);           // _core.pyx:379
+    a.disc = std::exp(-m->r * pr->maturity);               // engine.py:50
+    a.disc_up = std::exp(-(m->r + a.h_r) * pr->maturity);
+    a.disc_dn = std::exp(-(m->r - a.h_r) * pr->maturity);
+    a.n_steps = sim->n_steps;
+    a.n_avg = (int)pr->n_avg;
+    a.n_sim = (int)pr->avg_idx[pr->n_avg - 1];
+    bool every = (long long)a.n_sim == pr->n_avg;          // 1..n_sim all fixings
+    a.fix_mode = pr->n_avg == 1 ? hmc::kFixLast : (every ? hmc::kFixEvery : hmc::kFixTable);
+    a.is_asian = pr->style == HMC_STYLE_ASIAN;
+    a.is_call = pr->right == HMC_CALL;
+    a.want_greeks = sim->want_greeks ? 1 : 0;
+    a.milstein = sim->scheme == HMC_SCHEME_MILSTEIN;
+    a.sampler = sim->sampler;
+    a.n_runs = sim->n_runs;
+    a.n_paths = sim->n_paths;
+    a.path_lo = sim->path_lo;
+    a.path_hi = sim->path_hi;
+    a.root_key = hmc_root_key(sim->seed);
+    const uint32_t k0 = (uint32_t)a.root_key, k1 = (uint32_t)(a.root_key >> 32);
+    for (int i = 0; i < 10; ++i) {
+        a.rk0[i] = k0 + (uint32_t)i * 0x9E3779B9u;
+        a.rk1[i] = k1 + (uint32_t)i * 0xBB67AE85u;
+    }
+    a.sobol_dim = 2 * sim->n_steps;
+    fill_fp32_constants(a);
+
+    std::vector<unsigned char> fix((size_t)sim->n_steps + 1, 0);
+    for (long long i = 0; i < pr->n_avg; ++i) fix[pr->avg_idx[i]] = 1;
+    build_steps(sim->n_steps, pr->maturity, a.h_r, fix.data(), P);
+
+    const long long n = sim->path_hi - sim->path_lo;
+    P.n_tiles = n_tiles_of(n);
+    P.n_chunks = n_chunks_of(n);
+    size_t off = align_up((size_t)sim->n_runs * P.n_tiles * HMC_NW * sizeof(double));
+    P.off_st64 = off;
+    off += align_up(P.st64.size() * sizeof(StepD));
+    P.off_st32 = off;
+    off += align_up(P.st32.size() * sizeof(float4));
+    P.off_sobol = off;
+    if (sim->sampler == HMC_SAMPLER_SOBOL && !sim->sobol_v_on_device)
+        off += align_up((size_t)30 * a.sobol_dim * sizeof(uint32_t));
+    P.bytes = off;
+    return HMC_OK;
+}
+
+}  // namespace
+
+namespace hmc {
+
+__global__ void tiles_to_chunks_kernel(const double* __restrict__ tiles, long long n_tiles,
+                                       double* __restrict__ chunks, long long n_chunks) {
+    const int w = threadIdx.x;
+    if (w >= kNW) return;
+    const int run = blockIdx.y;
+    const long long c = blockIdx.x;
+    const long long t0 = c * HMC_CHUNK_TILES;
+    const long long t1 = t0 + HMC_CHUNK_TILES < n_tiles ? t0 + HMC_CHUNK_TILES : n_tiles;
+    const double* src = tiles + (size_t)run * n_tiles * kNW;
+    double s = 0.0;
+    for (long long t = t0; t < t1; ++t) s += src[t * kNW + w];
+    chunks[((size_t)run * n_chunks + c) * kNW + w] = s;
+}
+
+// Neumaier-compensated sequential sum over chunks in global path order
+__global__ void chunks_to_runs_kernel(const double* __restrict__ chunks, long long n_chunks,
+                                      double* __restrict__ out) {
+    const int w = threadIdx.x;
+    if (w >= kNW) return;
+    const int run = blockIdx.x;
+    const double* src = chunks + (size_t)run * n_chunks * kNW;
+    double s = 0.0, c = 0.0;
+    for (long long i = 0; i < n_chunks; ++i) {
+        const double x = src[i * kNW + w];
+        const double t = s + x;
+        if (fabs(s) >= fabs(x))
+            c += (s - t) + x;
+        else
+            c += (x - t) + s;
+        s = t;
+    }
+    out[(size_t)run * kNW + w] = s + c;
+}
+
+cudaError_t launch_tiles_to_chunks(const double* d_tiles, long long n_tiles, int n_runs,
+                                   double* d_chunks, long long n_chunks, cudaStream_t s) {
+    tiles_to_chunks_kernel<<<dim3((unsigned)n_chunks, (unsigned)n_runs), 32, 0, s>>>(
+        d_tiles, n_tiles, d_chunks, n_chunks);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_chunks_to_runs(const double* d_chunks, long long n_chunks, int n_runs,
+                                  double* d_out, cudaStream_t s) {
+    chunks_to_runs_kernel<<<(unsigned)n_runs, 32, 0, s>>>(d_chunks, n_chunks, d_out);
+    return cudaGetLastError();
+}
+
+}  // namespace hmc
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int hmc_abi_version(void) { return HMC_ABI_VERSION; }
+
+const char* hmc_last_error(void) { return g_err.c_str(); }
+
+int hmc_device_count(int32_t* count) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+        if (count) *count = 0;
+        cudaGetLastError();
+        return fail(HMC_E_NODEVICE, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+    }
+    if (count) *count = n;
+    return HMC_OK;
+}
+
+uint64_t hmc_root_key(uint64_t seed) { return hmc::mix64(seed ^ 0x8CB92BA72F3D8DD7ULL); }
+
+uint64_t hmc_derive_key(uint64_t parent, uint64_t index) { return hmc::derive(parent, index); }
+
+int64_t hmc_chunks_in_slice(const hmc_sim* sim) {
+    if (!sim || sim->path_hi <= sim->path_lo) return 0;
+    return n_chunks_of(sim->path_hi - sim->path_lo);
+}
+
+int64_t hmc_workspace_bytes(const hmc_sim* sim) {
+    if (!sim || sim->path_hi <= sim->path_lo || sim->n_steps < 1 || sim->n_runs < 1) return 0;
+    const long long n = sim->path_hi - sim->path_lo;
+    size_t b = align_up((size_t)sim->n_runs * n_tiles_of(n) * HMC_NW * sizeof(double));
+    b += align_up(((size_t)sim->n_steps + 1) * sizeof(StepD));
+    b += align_up(((size_t)sim->n_steps + 1) * sizeof(float4));
+    if (sim->sampler == HMC_SAMPLER_SOBOL && !sim->sobol_v_on_device)
+        b += align_up((size_t)30 * 2 * sim->n_steps * sizeof(uint32_t));
+    return (int64_t)b;
+}
+
+int hmc_greeks_chunks(const hmc_model* model, const hmc_product* product, const hmc_sim* sim,
+                      double* d_chunks, void* d_work, void* stream) {
+    Prepared P;
+    int rc = prepare(model, product, sim, P);
+    if (rc) return rc;
+    if (!d_chunks || !d_work) return fail(HMC_E_INVALID, "d_chunks / d_work is NULL");
+    cudaStream_t s = (cudaStream_t)stream;
+    char* w = (char*)d_work;
+    double* d_tiles = (double*)w;
+    HMC_CK(cudaMemcpyAsync(w + P.off_st64, P.st64.data(), P.st64.size() * sizeof(StepD),
+                           cudaMemcpyHostToDevice, s));
+    HMC_CK(cudaMemcpyAsync(w + P.off_st32, P.st32.data(), P.st32.size() * sizeof(float4),
+                           cudaMemcpyHostToDevice, s));
+    P.a.steps64 = (const StepD*)(w + P.off_st64);
+    P.a.steps32 = (const float4*)(w + P.off_st32);
+    if (sim->sampler == HMC_SAMPLER_SOBOL) {
+        if (sim->sobol_v_on_device) {
+            P.a.sobol_v = sim->sobol_v;
+        } else {
+            HMC_CK(cudaMemcpyAsync(w + P.off_sobol, sim->sobol_v,
+                                   (size_t)30 * P.a.sobol_dim * sizeof(uint32_t),
+                                   cudaMemcpyHostToDevice, s));
+            P.a.sobol_v = (const uint32_t*)(w + P.off_sobol);
+        }
+    }
+    if (sim->precision == HMC_PREC_FP64)
+        HMC_CK(hmc::launch_replay_greeks(P.a, d_tiles, P.n_tiles, s));
+    else
+        HMC_CK(hmc::launch_fast_greeks(P.a, d_tiles, P.n_tiles, s));
+    HMC_CK(hmc::launch_tiles_to_chunks(d_tiles, P.n_tiles, sim->n_runs, d_chunks, P.n_chunks, s));
+    return HMC_OK;
+}
+
+int hmc_reduce_chunks(const double* d_chunks, int32_t n_runs, int64_t n_chunks, double* d_out,
+                      void* stream) {
+    if (!d_chunks || !d_out || n_runs < 1 || n_chunks < 1)
+        return fail(HMC_E_INVALID, "bad reduce arguments");
+    HMC_CK(hmc::launch_chunks_to_runs(d_chunks, n_chunks, n_runs, d_out, (cudaStream_t)stream));
+    return HMC_OK;
+}
+
+int hmc_greeks(const hmc_model* model, const hmc_product* product, const hmc_sim* sim_in,
+               double* h_out, int32_t device) {
+    if (!sim_in || !h_out) return fail(HMC_E_INVALID, "sim / h_out is NULL");
+    hmc_sim sim = *sim_in;
+    sim.path_lo = 0;
+    sim.path_hi = sim.n_paths;
+    Prepared P;
+    int rc = prepare(model, product, &sim, P);
+    if (rc) return rc;
+    HMC_CK(cudaSetDevice(device));
+    cudaStream_t s;
+    HMC_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    const size_t work = (size_t)hmc_workspace_bytes(&sim);
+    const size_t chunk_bytes = (size_t)sim.n_runs * P.n_chunks * HMC_NW * sizeof(double);
+    const size_t out_bytes = (size_t)sim.n_runs * HMC_NW * sizeof(double);
+    char* buf = nullptr;
+    cudaError_t e = cudaMallocAsync((void**)&buf, work + align_up(chunk_bytes) + out_bytes, s);
+    if (e == cudaSuccess) {
+        double* d_chunks = (double*)(buf + work);
+        double* d_out = (double*)(buf + work + align_up(chunk_bytes));
+        rc = hmc_greeks_chunks(model, product, &sim, d_chunks, buf, s);
+        if (rc == HMC_OK) rc = hmc_reduce_chunks(d_chunks, sim.n_runs, P.n_chunks, d_out, s);
+        if (rc == HMC_OK) {
+            e = cudaMemcpyAsync(h_out, d_out, out_bytes, cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        }
+        cudaFreeAsync(buf, s);
+    }
+    cudaError_t e2 = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    if (rc) return rc;
+    HMC_CK(e);
+    HMC_CK(e2);
+    return HMC_OK;
+}
+
+int hmc_discretised_batch_f64(const hmc_model* model, double s0, double T, int32_t n_steps,
+                              int32_t milstein, int64_t path_lo, int64_t path_hi,
+                              uint64_t key_run, const double* uniforms, const int64_t* avg_idx,
+                              int64_t n_avg, double* out, int32_t device) {
+    int rc = check_model(model);
+    if (rc) return rc;
+    if (n_steps < 1 || !(T > 0.0) || !(s0 > 0.0)) return fail(HMC_E_INVALID, "need n_steps >= 1, T > 0, s0 > 0");
+    if (path_hi < path_lo) return fail(HMC_E_INVALID, "path_hi < path_lo");
+    if (!avg_idx || n_avg < 1) return fail(HMC_E_INVALID, "avg_idx must hold >= 1 index");
+    for (int64_t i = 0; i < n_avg; ++i)
+        if (avg_idx[i] < 0 || avg_idx[i] > n_steps) return fail(HMC_E_INVALID, "avg index outside [0, n_steps]");
+    const long long n = path_hi - path_lo;
+    if (n == 0) return HMC_OK;
+    if (!out) return fail(HMC_E_INVALID, "out is NULL");
+
+    Prepared P;
+    KernelArgs& a = P.a;
+    a.kappa = model->kappa; a.theta = model->theta; a.sigma = model->sigma;
+    a.rho = model->rho; a.r = model->r; a.v0 = model->v0;
+    a.s0 = s0; a.T = T;
+    a.dt = T / n_steps;
+    a.sq1mr2 = std::sqrt(1.0 - model->rho * model->rho);
+    a.n_steps = n_steps;
+    a.n_avg = (int)n_avg;  // the reference divides by len(avg_idx) (_core.pyx:370)
+    a.milstein = milstein ? 1 : 0;
+    a.path_lo = path_lo;
+    a.path_hi = path_hi;
+    std::vector<unsigned char> fix((size_t)n_steps + 1, 0);
+    for (int64_t i = 0; i < n_avg; ++i) fix[avg_idx[i]] = 1;
+    build_steps(n_steps, T, 0.0, fix.data(), P);
+
+    HMC_CK(cudaSetDevice(device));
+    cudaStream_t s;
+    HMC_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    const size_t ub = uniforms ? (size_t)n * 2 * n_steps * sizeof(double) : 0;
+    const size_t ob = (size_t)n * 3 * sizeof(double);
+    const size_t tb = P.st64.size() * sizeof(StepD);
+    char* buf = nullptr;
+    cudaError_t e = cudaMallocAsync((void**)&buf, align_up(ub) + align_up(ob) + tb, s);
+    if (e == cudaSuccess) {
+        double* d_u = uniforms ? (double*)buf : nullptr;
+        double* d_out = (double*)(buf + align_up(ub));
+        StepD* d_tab = (StepD*)(buf + align_up(ub) + align_up(ob));
+        if (uniforms) e = cudaMemcpyAsync(d_u, uniforms, ub, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d_tab, P.st64.data(), tb, cudaMemcpyHostToDevice, s);
+        a.steps64 = d_tab;
+        if (e == cudaSuccess) e = hmc::launch_replay_batch(a, key_run, d_u, d_out, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(out, d_out, ob, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        cudaFreeAsync(buf, s);
+    }
+    cudaError_t e2 = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    HMC_CK(e);
+    HMC_CK(e2);
+    return HMC_OK;
+}
+
+// Bratley-Fox / Joe-Kuo recurrence on the m-values, then the 2^(bits-1-b)
+// column scaling -- the construction scipy.stats.qmc.Sobol uses for its
+// unscrambled 30-bit direction numbers.
+int hmc_sobol_init_directions(const int64_t* poly, const int64_t* vinit, int32_t dim, uint32_t* v_out) {
+    const int bits = 30;
+    if (!poly || !vinit || !v_out || dim < 1 || dim > 21201)
+        return fail(HMC_E_INVALID, "bad sobol direction arguments");
+    std::vector<uint64_t> row(bits);
+    for (int d = 0; d < dim; ++d) {
+        if (d == 0) {
+            for (int b = 0; b < bits; ++b) row[b] = 1;
+        } else {
+            const uint64_t p = (uint64_t)poly[d];
+            int m = 0;
+            while ((p >> (m + 1)) != 0) ++m;  // degree = bit_length - 1
+            if (m < 1 || m > 18) return fail(HMC_E_INVALID, "bad sobol polynomial");
+            for (int j = 0; j < m && j < bits; ++j) row[j] = (uint64_t)vinit[(size_t)d * 18 + j];
+            for (int j = m; j < bits; ++j) {
+                uint64_t nv = row[j - m];
+                uint64_t pow2 = 1;
+                for (int k = 0; k < m; ++k) {
+                    pow2 <<= 1;
+                    if ((p >> (m - 1 - k)) & 1) nv ^= pow2 * row[j - k - 1];
+                }
+                row[j] = nv;
+            }
+        }
+        for (int b = 0; b < bits; ++b)
+            v_out[(size_t)b * dim + d] = (uint32_t)(row[b] << (bits - 1 - b));
+    }
+    return HMC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,199 @@
+// hmc_device.cuh -- device building blocks shared by the sm_100a path kernels.
+//
+//   * KernelArgs: everything a path kernel reads (by value -> constant bank)
+//   * Philox4x32-10 counter RNG (production stream)
+//   * SplitMix64 counter RNG + Acklam/Halley inverse normal in fp64
+//     (the reference stream, rng.py:38-132 / _core.pyx:57-109)
+//   * Gray-code Sobol coordinate (scipy.stats.qmc.Sobol, unscrambled, 30 bit)
+//   * fixed-order tile reduction of per-path quantities to fp64 partials
+#pragma once
+
+#include <cstdint>
+
+#include "../../include/hmc.h"
+
+namespace hmc {
+
+constexpr int kTile = HMC_TILE;
+constexpr int kNQ = HMC_NQ;
+constexpr int kNW = HMC_NW;
+constexpr int kWarps = kTile / 32;
+constexpr int kSobolBits = 30;
+
+enum FixMode : int {
+    kFixLast = 0,   // one fixing at the last simulated step (european)
+    kFixEvery = 1,  // every step is a fixing date (daily-fixing asian)
+    kFixTable = 2   // fixing flags from the step table
+};
+
+// Per-step table entry, built on the host in fp64 (t_k = k*T/n_steps exactly
+// as _core.pyx:406), also shipped as fp32.
+//   x = t_k, y = expm1(+h_r t_k), z = expm1(-h_r t_k), w = 1 if k is a fixing
+struct StepD {
+    double t, e1p, e1m, fix;
+};
+
+struct KernelArgs {
+    // model (HestonParams) and product (OptionSpec)
+    double kappa, theta, sigma, rho, r, v0;
+    double s0, T, K;
+    double v0_up, v0_dn, h_spot, h_r;
+    double dt, sq1mr2;
+    double disc, disc_up, disc_dn;  // exp(-r T), exp(-(r +- h_r) T)  (host libm)
+    int n_steps;     // grid size (dt = T / n_steps)
+    int n_sim;       // steps actually simulated (last fixing for asians)
+    int n_avg;       // number of fixing dates
+    int fix_mode;
+    int is_asian, is_call, want_greeks, milstein;
+    int sampler;
+    int n_runs;
+    long long n_paths, path_lo, path_hi;
+    // pseudo: Philox round keys (fp32 path) / SplitMix64 root key (fp64 path)
+    uint32_t rk0[10], rk1[10];
+    unsigned long long root_key;
+    // tables (device pointers)
+    const StepD* steps64;       // [n_steps + 1]
+    const float4* steps32;      // [n_steps + 1]
+    const uint32_t* sobol_v;    // [30][sobol_dim]
+    int sobol_dim;
+    // fp32 derived constants (host-computed in fp64, rounded once)
+    float f_omkdt;   // 1 - kappa dt
+    float f_ck0;     // kappa theta dt - milstein * sigma^2 dt / 4
+    float f_cmil;    // milstein * sigma^2 / 4
+    float f_sigma;
+    float f_nhdt2;   // -0.5 dt log2(e)
+    float f_bm;      // -2 ln(2) dt     (Box-Muller radius^2 per lg2 unit)
+    float f_rl2;     // r log2(e)
+    float f_l2s0;    // log2(S0)
+    float f_log2e;
+    float f_rho, f_sq1mr2;
+    float f_sqdt;    // sqrt(dt)
+};
+
+// ---------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al., SC'11).  Counter = (step pair, path lo, path
+// hi, run); key = root_key(seed) so the 10 round keys are kernel parameters
+// (constant-bank operands, no registers).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2,
+                                               uint32_t c3, const KernelArgs& a) {
+#pragma unroll
+    for (int i = 0; i < 10; ++i) {
+        const unsigned long long p0 = (unsigned long long)0xD2511F53u * c0;
+        const unsigned long long p1 = (unsigned long long)0xCD9E8D57u * c2;
+        const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        c0 = hi1 ^ c1 ^ a.rk0[i];
+        c1 = lo1;
+        c2 = hi0 ^ c3 ^ a.rk1[i];
+        c3 = lo0;
+    }
+    return make_uint4(c0, c1, c2, c3);
+}
+
+// ---------------------------------------------------------------------------
+// Reference stream: SplitMix64 (rng.py:38-65, _core.pyx:57-68)
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ unsigned long long derive(unsigned long long parent,
+                                                              unsigned long long index) {
+    return mix64(parent ^ mix64(index + 0xD1B54A32D192ED03ULL));
+}
+__host__ __device__ __forceinline__ double uniform_at(unsigned long long key,
+                                                      unsigned long long i) {
+    return (double)(mix64(key + (i + 1) * 0x9E3779B97F4A7C15ULL) >> 11) *
+           (1.0 / 9007199254740992.0);
+}
+
+// ---------------------------------------------------------------------------
+// Sobol coordinate d of Gray-code point n: XOR of v[b][d] over the set bits
+// of gray(n) = n ^ (n >> 1), as 30-bit integer.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t sobol_coord(uint32_t gray, const uint32_t* __restrict__ v,
+                                                int dim, int d) {
+    uint32_t x = 0;
+#pragma unroll
+    for (int b = 0; b < kSobolBits; ++b) {
+        if ((gray >> b) & 1u) x ^= __ldg(v + b * dim + d);
+    }
+    return x;
+}
+
+// ---------------------------------------------------------------------------
+// Fixed-order tile reduction: every thread holds kNQ per-path values; write
+// {sum x, sum x^2} per quantity for the tile.  Butterfly shuffles then warps
+// in index order -- deterministic for a given tile content.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void tile_reduce_store(const double (&q)[kNQ], double* __restrict__ out) {
+    __shared__ double red[kWarps][kNW];
+    double w[kNW];
+#pragma unroll
+    for (int i = 0; i < kNQ; ++i) {
+        w[2 * i] = q[i];
+        w[2 * i + 1] = q[i] * q[i];
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+#pragma unroll
+        for (int i = 0; i < kNW; ++i) w[i] += __shfl_xor_sync(0xffffffffu, w[i], off);
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < kNW; ++i) red[warp][i] = w[i];
+    }
+    __syncthreads();
+    if (threadIdx.x < kNW) {
+        double s = red[0][threadIdx.x];
+#pragma unroll
+        for (int k = 1; k < kWarps; ++k) s += red[k][threadIdx.x];
+        out[threadIdx.x] = s;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Per-path estimators (engine.py:47-68 for price / pathwise Delta / pathwise
+// Rho; CRN finite differences for the rest, test_products.py:101-137).
+//   A      underlying: average over fixings (asian) or S_T (european)
+//   tw     (1/N) sum S_k t_k                     (Asian pathwise Rho)
+//   Au/Ad  underlyings of the v0 +/- trajectories (Vega)
+//   Rp/Rm  underlyings under r +/- h_r by exact rescaling:
+//          S_k(r+h) = S_k(r) e^{h t_k}  (r enters the log-Euler drift only)
+// S0 +/- h is an exact rescaling too: S_k(S0+h) = S_k (S0+h)/S0, so the
+// pathwise Delta of the bumped path equals disc*A/S0 on its exercise set.
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T pos_part(T x) {
+    return x > T(0) ? x : T(0);
+}
+
+template <typename T>
+__device__ __forceinline__ void greeks_epilogue(const KernelArgs& a, T A, T tw, T Au, T Ad,
+                                                T Rp, T Rm, double (&q)[kNQ]) {
+    const T K = (T)a.K, disc = (T)a.disc;
+    auto payoff = [&](T x, T d) -> T { return a.is_call ? d * pos_part(x - K) : d * pos_part(K - x); };
+    q[HMC_Q_PRICE] = (double)payoff(A, disc);
+#pragma unroll
+    for (int i = 1; i < kNQ; ++i) q[i] = 0.0;
+    if (!a.want_greeks) return;
+    const T S0 = (T)a.s0, h = (T)a.h_spot;
+    const bool itm = A > K;
+    if (itm) {
+        q[HMC_Q_DELTA] = (double)(disc * A / S0);
+        q[HMC_Q_RHO] = a.is_asian ? (double)(disc * (tw - (T)a.T * (A - K)))
+                                  : (double)(disc * K * (T)a.T);
+    }
+    const T Aup = A * ((S0 + h) / S0), Adn = A * ((S0 - h) / S0);
+    const T ind = (T)((Aup > K) ? 1 : 0) - (T)((Adn > K) ? 1 : 0);
+    q[HMC_Q_GAMMA] = (double)(ind * (disc * A / S0) / (T(2) * h));
+    q[HMC_Q_DELTA_FD] = (double)((payoff(Aup, disc) - payoff(Adn, disc)) / (T(2) * h));
+    q[HMC_Q_VEGA] = (double)((payoff(Au, disc) - payoff(Ad, disc)) / (T)(a.v0_up - a.v0_dn));
+    q[HMC_Q_RHO_FD] = (double)((payoff(Rp, (T)a.disc_up) - payoff(Rm, (T)a.disc_dn)) /
+                               (T(2) * (T)a.h_r));
+}
+
+}  // namespace hmc

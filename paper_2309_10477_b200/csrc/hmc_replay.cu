@@ -1,0 +1,202 @@
+// hmc_replay.cu -- fp64 "replay" kernels: the reference's own random stream
+// and arithmetic, one path per thread, on sm_100a.
+//
+// Compiled with -fmad=false: the reference's C build (-O3, x86-64 baseline,
+// pkg/setup.py:11) has no FMA, so the GPU follows the same rounding sequence
+// operation for operation (_core.pyx:384-411).  Remaining differences are the
+// last-ulp behaviour of CUDA's exp/log/erfc vs glibc's, i.e. ~1e-16 relative
+// per step; the parity gate is 1e-12 per path (tests/test_gpu_replay.py).
+//
+//   replay_batch_kernel   backend discretised_batch: per-path (s_T, avg, tw)
+//   replay_greeks_kernel  engine path: base + v0 +/- trajectories per thread,
+//                         per-path estimators, fp64 tile partials
+#include <cuda_runtime.h>
+
+#include "hmc_device.cuh"
+#include "hmc_launch.h"
+
+namespace hmc {
+
+// Acklam rational approximation + one Halley step on erfc
+// (_core.pyx:75-109, rng.py:82-132)
+__device__ __noinline__ double ndtri_ref(double u) {
+    double q, s, num, den, x, e, corr, p, sign;
+    if (u < 1e-300) u = 1e-300;
+    if (u > 1.0 - 1e-16) u = 1.0 - 1e-16;
+    if (0.02425 <= u && u <= 0.97575) {
+        q = u - 0.5;
+        s = q * q;
+        num = ((((-3.969683028665376e+01 * s + 2.209460984245205e+02) * s
+                 - 2.759285104469687e+02) * s + 1.383577518672690e+02) * s
+               - 3.066479806614716e+01) * s + 2.506628277459239e+00;
+        den = ((((-5.447609879822406e+01 * s + 1.615858368580409e+02) * s
+                 - 1.556989798598866e+02) * s + 6.680131188771972e+01) * s
+               - 1.328068155288572e+01) * s + 1.0;
+        x = q * num / den;
+    } else {
+        if (u < 0.02425) {
+            p = u;
+            sign = 1.0;
+        } else {
+            p = 1.0 - u;
+            sign = -1.0;
+        }
+        q = sqrt(-2.0 * log(p));
+        num = ((((-7.784894002430293e-03 * q - 3.223964580411365e-01) * q
+                 - 2.400758277161838e+00) * q - 2.549732539343734e+00) * q
+               + 4.374664141464968e+00) * q + 2.938163982698783e+00;
+        den = (((7.784695709041462e-03 * q + 3.224671290700398e-01) * q
+                + 2.445134137142996e+00) * q + 3.754408661907416e+00) * q + 1.0;
+        x = sign * num / den;
+    }
+    e = 0.5 * erfc(-x / sqrt(2.0)) - u;
+    corr = e * 2.5066282746310002 * exp(0.5 * x * x);
+    x -= corr / (1.0 + 0.5 * x * corr);
+    return x;
+}
+
+struct TrajD {
+    double s, v, ps, tw;
+};
+
+// one Euler/Milstein full-truncation step (_core.pyx:399-404)
+__device__ __forceinline__ void ref_step(TrajD& t, double z1, double z2, const KernelArgs& a) {
+    const double sqv = sqrt(t.v * a.dt);
+    t.s = t.s * exp((a.r - 0.5 * t.v) * a.dt + sqv * z1);
+    double v_new = t.v + a.kappa * (a.theta - t.v) * a.dt + a.sigma * sqv * z2;
+    if (a.milstein) v_new = v_new + 0.25 * a.sigma * a.sigma * a.dt * (z2 * z2 - 1.0);
+    t.v = v_new > 0.0 ? v_new : 0.0;
+}
+
+// the two uniforms of step k (1-based) for this path: reference layout
+// u[2(k-1)] -> asset, u[2(k-1)+1] -> variance (_core.pyx:391-396)
+struct RefDraws {
+    int sampler;
+    unsigned long long key;         // pseudo: per-path main key
+    uint32_t gray;                  // sobol: Gray code of the point index
+    const uint32_t* v;
+    int dim;
+    const double* row;              // supplied uniforms (replay batch) or null
+    __device__ __forceinline__ void get(int k, double& u1, double& u2) const {
+        const int i = 2 * (k - 1);
+        if (row) {
+            u1 = row[i];
+            u2 = row[i + 1];
+        } else if (sampler == HMC_SAMPLER_PSEUDO) {
+            u1 = uniform_at(key, (unsigned long long)i);
+            u2 = uniform_at(key, (unsigned long long)(i + 1));
+        } else {
+            u1 = (double)sobol_coord(gray, v, dim, i) * (1.0 / 1073741824.0);
+            u2 = (double)sobol_coord(gray, v, dim, i + 1) * (1.0 / 1073741824.0);
+        }
+    }
+};
+
+__global__ void __launch_bounds__(kTile) replay_batch_kernel(const KernelArgs a,
+                                                             unsigned long long key_run,
+                                                             const double* __restrict__ uniforms,
+                                                             double* __restrict__ out) {
+    const long long n = a.path_hi - a.path_lo;
+    const long long i = (long long)blockIdx.x * kTile + threadIdx.x;
+    if (i >= n) return;
+    RefDraws dr{};
+    dr.sampler = HMC_SAMPLER_PSEUDO;
+    dr.key = derive(derive(key_run, (unsigned long long)(a.path_lo + i)), 0ULL);
+    dr.row = uniforms ? uniforms + (size_t)i * 2 * a.n_steps : nullptr;
+    TrajD t{a.s0, a.v0, 0.0, 0.0};
+    for (int k = 1; k <= a.n_steps; ++k) {
+        double u1, u2;
+        dr.get(k, u1, u2);
+        const double z1 = ndtri_ref(u1);
+        const double z2 = a.rho * z1 + a.sq1mr2 * ndtri_ref(u2);
+        ref_step(t, z1, z2, a);
+        const StepD st = a.steps64[k];
+        if (st.fix != 0.0) {
+            t.ps += t.s;
+            t.tw += t.s * st.t;
+        }
+    }
+    out[3 * i + 0] = t.s;
+    out[3 * i + 1] = t.ps / a.n_avg;
+    out[3 * i + 2] = t.tw / a.n_avg;
+}
+
+template <bool GREEKS>
+__global__ void __launch_bounds__(kTile) replay_greeks_kernel(const KernelArgs a,
+                                                              double* __restrict__ tiles,
+                                                              long long n_tiles) {
+    const int run = blockIdx.y;
+    const long long path = a.path_lo + (long long)blockIdx.x * kTile + threadIdx.x;
+    const bool live = path < a.path_hi;
+    const long long p = live ? path : a.path_lo;
+    RefDraws dr{};
+    dr.sampler = a.sampler;
+    if (a.sampler == HMC_SAMPLER_PSEUDO) {
+        // engine.py:96 key_run = derive(root(seed), run); _core.pyx:385
+        const unsigned long long key_run = derive(a.root_key, (unsigned long long)run);
+        dr.key = derive(derive(key_run, (unsigned long long)p), 0ULL);
+    } else {
+        // engine.py:100: run r uses Sobol rows 1 + r*n_paths + path
+        const uint32_t n = (uint32_t)(1 + (long long)run * a.n_paths + p);
+        dr.gray = n ^ (n >> 1);
+        dr.v = a.sobol_v;
+        dr.dim = a.sobol_dim;
+    }
+    TrajD t0{a.s0, a.v0, 0.0, 0.0};
+    TrajD tu{a.s0, a.v0_up, 0.0, 0.0};
+    TrajD td{a.s0, a.v0_dn, 0.0, 0.0};
+    double dp = 0.0, dm = 0.0;
+    for (int k = 1; k <= a.n_sim; ++k) {
+        double u1, u2;
+        dr.get(k, u1, u2);
+        const double z1 = ndtri_ref(u1);
+        const double z2 = a.rho * z1 + a.sq1mr2 * ndtri_ref(u2);
+        ref_step(t0, z1, z2, a);
+        if (GREEKS) {
+            ref_step(tu, z1, z2, a);
+            ref_step(td, z1, z2, a);
+        }
+        const StepD st = a.steps64[k];
+        if (st.fix != 0.0) {
+            t0.ps += t0.s;
+            t0.tw += t0.s * st.t;
+            if (GREEKS) {
+                tu.ps += tu.s;
+                td.ps += td.s;
+                dp += t0.s * st.e1p;
+                dm += t0.s * st.e1m;
+            }
+        }
+    }
+    // european: the one fixing is t_n = T, so ps = s_T and the reference's
+    // obs[:, 0] == obs[:, 1] (engine.py:51)
+    const double A = t0.ps / a.n_avg;
+    double q[kNQ];
+    greeks_epilogue<double>(a, A, t0.tw / a.n_avg, tu.ps / a.n_avg, td.ps / a.n_avg,
+                            A + dp / a.n_avg, A + dm / a.n_avg, q);
+    if (!live) {
+#pragma unroll
+        for (int i = 0; i < kNQ; ++i) q[i] = 0.0;
+    }
+    tile_reduce_store(q, tiles + ((size_t)run * n_tiles + blockIdx.x) * kNW);
+}
+
+cudaError_t launch_replay_batch(const KernelArgs& a, unsigned long long key_run,
+                                const double* d_uniforms, double* d_out, cudaStream_t s) {
+    const long long n = a.path_hi - a.path_lo;
+    const unsigned grid = (unsigned)((n + kTile - 1) / kTile);
+    replay_batch_kernel<<<grid, kTile, 0, s>>>(a, key_run, d_uniforms, d_out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_replay_greeks(const KernelArgs& a, double* d_tiles, long long n_tiles,
+                                 cudaStream_t s) {
+    dim3 grid((unsigned)n_tiles, (unsigned)a.n_runs);
+    if (a.want_greeks)
+        replay_greeks_kernel<true><<<grid, kTile, 0, s>>>(a, d_tiles, n_tiles);
+    else
+        replay_greeks_kernel<false><<<grid, kTile, 0, s>>>(a, d_tiles, n_tiles);
+    return cudaGetLastError();
+}
+
+}  // namespace hmc

@@ -1,0 +1,291 @@
+"""GPU engine parity: the drop-in ``price`` / ``greeks`` / ``run_experiment``.
+
+* fp64 replay precision: per-run values equal the reference engine's
+  (golden, produced by the reference) to 1e-12 relative for price / Delta /
+  Rho and to 1e-9 for the CRN finite differences (FD quotients amplify
+  last-ulp differences by 1/h).
+* fp32 production precision (Philox): independent-RNG estimates agree with
+  the reference's within 3 combined standard errors (north star, check (b)),
+  and European prices/Greeks with the Heston semi-analytic values and the
+  Broadie-Kaya exact baseline (check (c)).
+"""
+
+import ctypes
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import engine as oe
+from oracle.semi_analytic import call_greeks
+from conftest import spec_from
+from paper_2309_10477_b200 import (BENCH_PARAMS, HestonParams, OptionSpec, SimConfig,
+                                   UnsupportedProduct, daily_fixings, engine, greeks, price,
+                                   run_experiment)
+
+pytestmark = pytest.mark.gpu
+
+QN = ("price", "delta", "rho", "gamma", "vega", "delta_fd", "rho_fd")
+
+
+def _close_se(a, a_se, b, b_se, k=3.0, floor=0.0):
+    return abs(a - b) <= k * math.hypot(a_se, b_se) + floor
+
+
+class TestReplayPrecisionMatchesReferenceEngine:
+    def test_per_run_values(self, golden_engine):
+        for name, c in golden_engine.items():
+            p, spec = HestonParams(**c["params"]), spec_from(c["spec"])
+            cfg = SimConfig(precision="fp64", **c["config"])
+            s = price(p, spec, cfg)
+            np.testing.assert_allclose(s.per_run_values, c["price"], rtol=1e-12, err_msg=name)
+            if "greeks_delta" not in c:
+                continue
+            b = c["bumps"]
+            cfg = SimConfig(precision="fp64", bump_spot=b["h_spot"] / spec.spot,
+                            bump_v0=(b["v0_up"] - p.v0) / p.v0, bump_r=b["h_r"], **c["config"])
+            g = greeks(p, spec, cfg)
+            np.testing.assert_allclose(g["price"].per_run_values, c["greeks_price"], rtol=1e-12)
+            np.testing.assert_allclose(g["delta"].per_run_values, c["greeks_delta"], rtol=1e-12)
+            np.testing.assert_allclose(g["rho"].per_run_values, c["greeks_rho"], rtol=1e-12)
+            np.testing.assert_allclose(g["delta_fd"].per_run_values, c["fd_delta"], rtol=1e-9, atol=1e-10)
+            np.testing.assert_allclose(g["rho_fd"].per_run_values, c["fd_rho"], rtol=1e-9, atol=1e-8)
+            np.testing.assert_allclose(g["vega"].per_run_values, c["fd_vega"], rtol=1e-9, atol=1e-8)
+
+    def test_gamma_vs_oracle_fd(self, bench_params, euro_call):
+        cfg = SimConfig(scheme="milstein", n_paths=20000, n_steps=32, n_runs=2, seed=5,
+                        precision="fp64")
+        g = greeks(bench_params, euro_call, cfg)
+        bumps = engine.bump_sizes(bench_params, euro_call, cfg)
+        s = oe.greeks_sums(bench_params, euro_call, cfg, bumps, workers=8)
+        for q, name in enumerate(QN):
+            np.testing.assert_allclose(g[name].per_run_values, s[:, 2 * q] / cfg.n_paths,
+                                       rtol=1e-9, atol=1e-9, err_msg=name)
+
+
+class TestProductionPrecision:
+    def test_full_size_vs_reference_statistics(self, golden_stats):
+        """BASELINE params, 252 steps: fp32 Philox GPU at 2^22 paths vs the
+        reference's 2^20-path per-path statistics (same discretisation,
+        independent RNG) -- all seven quantities within 3 combined SE."""
+        p = HestonParams(**golden_stats["params"])
+        b = golden_stats["bumps"]
+        specs = {
+            "euro": OptionSpec("european", "call", 100.0, 1.0, 100.0),
+            "asian_daily": OptionSpec("asian_arithmetic", "call", 100.0, 1.0, 100.0,
+                                      averaging_times=daily_fixings(1.0, 252)),
+        }
+        cfg = SimConfig(scheme="milstein", n_paths=2**22, n_steps=252, n_runs=1, seed=7,
+                        bump_spot=b["h_spot"] / 100.0, bump_v0=(b["v0_up"] - p.v0) / p.v0,
+                        bump_r=b["h_r"])
+        for name, spec in specs.items():
+            g = greeks(p, spec, cfg)
+            for q in QN:
+                ref, ref_se = golden_stats[name][q]
+                assert _close_se(g[q].estimate, g[q].path_std_error, ref, ref_se), \
+                    (name, q, g[q].estimate, g[q].path_std_error, ref, ref_se)
+
+    def test_european_vs_semi_analytic(self):
+        p = HestonParams(**BENCH_PARAMS)
+        spec = OptionSpec("european", "call", 100.0, 1.0, 100.0)
+        cfg = SimConfig(scheme="milstein", n_paths=2**22, n_steps=252, n_runs=1, seed=11)
+        g = greeks(p, spec, cfg)
+        sa = call_greeks(100.0, 100.0, 1.0, p.r, p.kappa, p.theta, p.sigma, p.rho, p.v0)
+        for q in ("price", "delta", "rho"):
+            assert _close_se(g[q].estimate, g[q].path_std_error, sa[q], 0.0), (q, g[q].estimate, sa[q])
+        # FD gamma/vega carry an O(h^2) bump bias and a small time-step bias; 4 SE
+        for q in ("gamma", "vega"):
+            assert _close_se(g[q].estimate, g[q].path_std_error, sa[q], 0.0, k=4.0), \
+                (q, g[q].estimate, g[q].path_std_error, sa[q])
+
+    def test_european_vs_broadie_kaya(self, golden_stats):
+        p = HestonParams(**golden_stats["params"])
+        spec = OptionSpec("european", "call", 100.0, 1.0, 100.0)
+        s = price(p, spec, SimConfig(scheme="milstein", n_paths=2**22, n_steps=252, n_runs=1, seed=3))
+        bk, bk_se = golden_stats["bk_exact_euro"]["price"]
+        assert _close_se(s.estimate, s.path_std_error, bk, bk_se)
+
+    def test_paper_acceptance_values(self, params, euro_call, asian_call):
+        """Reference acceptance criteria 3-5 (tests/test_acceptance.py:67-132)
+        on the production path: Milstein 32k x 128 x 30 runs."""
+        cfg = SimConfig(scheme="milstein", n_paths=32000, n_steps=128, n_runs=30, seed=42)
+        g = greeks(params, euro_call, cfg)
+        assert abs(g["price"].estimate - 6.8061) <= 0.15
+        assert abs(g["delta"].estimate - 0.6958) <= 3 * g["delta"].std_error
+        assert abs(g["rho"].estimate - 62.7752) <= 3 * g["rho"].std_error
+        a = price(params, asian_call, cfg)
+        assert abs(a.estimate - 4.3840) <= 0.15
+
+    def test_timestep_plateau(self, params, euro_call):
+        grid = [SimConfig(scheme="milstein", n_paths=32000, n_steps=n, n_runs=30, seed=42)
+                for n in (32, 64, 128, 256)]
+        rows = run_experiment(grid, params, euro_call)
+        sums = {r["steps"]: r["summaries"]["price"] for r in rows}
+        for a in sums:
+            for b in sums:
+                if a < b:
+                    assert abs(sums[a].estimate - sums[b].estimate) <= \
+                        3 * max(sums[a].std_error, sums[b].std_error)
+
+    def test_black_scholes_limit(self, euro_call):
+        # reference criterion 8 (tests/test_acceptance.py:196-212)
+        from scipy.special import ndtr
+        p = HestonParams(kappa=6.21, theta=0.019, sigma=1e-6, rho=-0.7, r=0.0319, v0=0.010201)
+        tv = p.theta + (p.v0 - p.theta) * (1.0 - math.exp(-p.kappa)) / p.kappa
+        sq = math.sqrt(tv)
+        d1 = (math.log(1.0) + p.r + 0.5 * tv) / sq
+        bs = 100 * ndtr(d1) - 100 * math.exp(-p.r) * ndtr(d1 - sq)
+        for scheme in ("euler", "milstein"):
+            s = price(p, euro_call, SimConfig(scheme=scheme, n_paths=100_000, n_steps=128,
+                                               n_runs=10, seed=42))
+            assert abs(s.estimate - bs) <= 3 * s.std_error, (scheme, s.estimate, bs)
+
+    def test_put_call_parity(self, bench_params):
+        call = OptionSpec("european", "call", 105.0, 1.0, 100.0)
+        put = OptionSpec("european", "put", 105.0, 1.0, 100.0)
+        cfg = SimConfig(scheme="milstein", n_paths=8000, n_steps=64, n_runs=10, seed=77)
+        c, pt = price(bench_params, call, cfg), price(bench_params, put, cfg)
+        diffs = np.array(c.per_run_values) - np.array(pt.per_run_values)
+        target = 100.0 - 105.0 * math.exp(-bench_params.r)
+        se = diffs.std(ddof=1) / math.sqrt(len(diffs))
+        assert abs(diffs.mean() - target) < 3.0 * max(se, 1e-12)
+
+    @pytest.mark.parametrize("spec_name", ["euro_call", "asian_call"])
+    def test_pathwise_vs_fd_in_one_pass(self, params, spec_name, request):
+        """delta vs delta_fd and rho vs rho_fd from the same fused pass
+        (reference tests/test_products.py:101-125, CRN)."""
+        spec = request.getfixturevalue(spec_name)
+        g = greeks(params, spec, SimConfig(scheme="milstein", n_paths=8000, n_steps=64, n_runs=10,
+                                           seed=77))
+        for pw, fd, floor in (("delta", "delta_fd", 1e-4), ("rho", "rho_fd", 1e-2)):
+            diff = np.array(g[pw].per_run_values) - np.array(g[fd].per_run_values)
+            se = diff.std(ddof=1) / math.sqrt(len(diff))
+            assert abs(diff.mean()) < 3.0 * max(se, floor), (pw, diff.mean(), se)
+
+    def test_delta_to_discounted_forward_as_strike_vanishes(self, params):
+        spec = OptionSpec("european", "call", 1e-6, 1.0, 100.0)
+        g = greeks(params, spec, SimConfig(scheme="milstein", n_paths=20000, n_steps=64, n_runs=10,
+                                           seed=42))
+        d = g["delta"]
+        assert abs(d.estimate - 1.0) < 3.0 * d.std_error / math.sqrt(d.n_runs)
+
+
+class TestEngineContract:
+    def test_deterministic_repeat(self, params, euro_call):
+        cfg = SimConfig(scheme="milstein", n_paths=50000, n_steps=64, n_runs=3, seed=42)
+        a, b = greeks(params, euro_call, cfg), greeks(params, euro_call, cfg)
+        for q in QN:
+            assert a[q].per_run_values == b[q].per_run_values
+
+    def test_single_pass_greeks_match_price(self, params, euro_call, asian_call):
+        # reference tests/test_engine.py:39-42
+        for spec in (euro_call, asian_call):
+            for prec in ("fp32", "fp64"):
+                cfg = SimConfig(scheme="milstein", n_paths=8192, n_steps=32, n_runs=3, seed=42,
+                                precision=prec)
+                assert greeks(params, spec, cfg)["price"].per_run_values == \
+                    price(params, spec, cfg).per_run_values
+
+    def test_split_slices_bit_identical(self, bench_params):
+        """Two chunk-aligned slices reduced together == the whole job: the
+        property that makes multi-GPU results identical to 1-GPU results."""
+        import torch
+        from paper_2309_10477_b200 import _lib, parallel
+        spec = OptionSpec("asian_arithmetic", "call", 100.0, 1.0, 100.0,
+                          averaging_times=daily_fixings(1.0, 64))
+        cfg = SimConfig(scheme="milstein", n_paths=5 * 16384 + 1000, n_steps=64, n_runs=2, seed=9)
+        whole = engine.Job(bench_params, spec, cfg, True).run_device()
+        L = _lib.lib()
+        parts = []
+        for rank in range(3):
+            sl = parallel.shard(cfg.n_paths, rank, 3)
+            job = engine.Job(bench_params, spec, cfg, True)
+            job.sim.path_lo, job.sim.path_hi = sl.path_lo, sl.path_hi
+            loc = torch.zeros((cfg.n_runs, sl.n_chunks, _lib.HMC_NW), dtype=torch.float64, device="cuda")
+            work = torch.empty(L.hmc_workspace_bytes(ctypes.byref(job.sim)), dtype=torch.uint8, device="cuda")
+            _lib.check(L.hmc_greeks_chunks(ctypes.byref(job.model), ctypes.byref(job.product),
+                                           ctypes.byref(job.sim), ctypes.c_void_p(loc.data_ptr()),
+                                           ctypes.c_void_p(work.data_ptr()), None))
+            parts.append(loc)
+        full = torch.cat(parts, dim=1).contiguous()
+        out = torch.empty((cfg.n_runs, _lib.HMC_NW), dtype=torch.float64, device="cuda")
+        _lib.check(L.hmc_reduce_chunks(ctypes.c_void_p(full.data_ptr()), cfg.n_runs, full.shape[1],
+                                       ctypes.c_void_p(out.data_ptr()), None))
+        np.testing.assert_array_equal(out.cpu().numpy(), whole)
+
+    def test_c_abi_one_call_matches_engine(self, bench_params, euro_call):
+        from paper_2309_10477_b200 import _lib
+        cfg = SimConfig(scheme="milstein", n_paths=40000, n_steps=63, n_runs=2, seed=4)
+        job = engine.Job(bench_params, euro_call, cfg, True)
+        host = np.zeros((cfg.n_runs, _lib.HMC_NW))
+        _lib.check(_lib.lib().hmc_greeks(ctypes.byref(job.model), ctypes.byref(job.product),
+                                         ctypes.byref(job.sim),
+                                         host.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), 0))
+        np.testing.assert_array_equal(host, job.run_device())
+
+    def test_summary_fields(self, params, euro_call):
+        s = price(params, euro_call, SimConfig(scheme="milstein", n_paths=8192, n_steps=32, n_runs=5,
+                                               seed=42))
+        assert s.n_runs == 5 and s.n_paths == 8192 and len(s.per_run_values) == 5
+        assert s.estimate == pytest.approx(np.mean(s.per_run_values))
+        assert s.std_error == pytest.approx(np.std(s.per_run_values, ddof=1))
+        assert s.wall_ms > 0.0 and s.path_std_error > 0.0
+
+    def test_se_scaling(self, params, euro_call):
+        small = price(params, euro_call, SimConfig(scheme="milstein", n_paths=2000, n_steps=64,
+                                                   n_runs=30, seed=21))
+        large = price(params, euro_call, SimConfig(scheme="milstein", n_paths=8000, n_steps=64,
+                                                   n_runs=30, seed=21))
+        assert 0.35 < large.std_error / small.std_error < 0.65
+
+    @pytest.mark.parametrize("n_paths,n_steps", [(1, 1), (2, 3), (127, 5), (129, 7),
+                                                 (16385, 2), (100_000, 1)])
+    def test_ragged_sizes_vs_fp64(self, bench_params, n_paths, n_steps):
+        """Partial tiles / chunks and odd step counts (Philox tail): fp32
+        agrees with the fp64 replay within 3 SE."""
+        spec = OptionSpec("european", "call", 100.0, 1.0, 100.0)
+        a = price(bench_params, spec, SimConfig(scheme="milstein", n_paths=n_paths, n_steps=n_steps,
+                                                 n_runs=1, seed=1))
+        b = price(bench_params, spec, SimConfig(scheme="milstein", n_paths=n_paths, n_steps=n_steps,
+                                                 n_runs=1, seed=1, precision="fp64"))
+        assert np.isfinite(a.estimate)
+        if n_paths > 1000:
+            assert _close_se(a.estimate, a.path_std_error, b.estimate, b.path_std_error)
+
+    @pytest.mark.parametrize("over", [dict(v0=0.0), dict(rho=1.0), dict(rho=-1.0),
+                                      dict(sigma=2.0, theta=0.01)])
+    def test_edge_params_vs_oracle(self, over):
+        p = HestonParams(**{**BENCH_PARAMS, **over})
+        spec = OptionSpec("asian_arithmetic", "call", 100.0, 1.0, 100.0,
+                          averaging_times=daily_fixings(1.0, 32))
+        cfg = SimConfig(scheme="milstein", n_paths=2**17, n_steps=32, n_runs=1, seed=2)
+        g = greeks(p, spec, cfg)
+        s = oe.greeks_sums(p, spec, SimConfig(scheme="milstein", n_paths=2**15, n_steps=32, n_runs=1,
+                                              seed=3), engine.bump_sizes(p, spec, cfg), workers=8)
+        M = 2**15
+        for q, name in enumerate(QN):
+            mean = s[0, 2 * q] / M
+            se = math.sqrt(max(s[0, 2 * q + 1] / M - mean * mean, 0.0) / (M - 1))
+            assert np.isfinite(g[name].estimate)
+            assert _close_se(g[name].estimate, g[name].path_std_error, mean, se, k=4.0, floor=1e-6), \
+                (over, name, g[name].estimate, mean, se)
+
+
+class TestSobol:
+    def test_fp32_sobol_vs_reference_engine(self, golden_engine):
+        c = golden_engine["paper_asian_sobol"]
+        p, spec = HestonParams(**c["params"]), spec_from(c["spec"])
+        cfg = SimConfig(**c["config"])
+        g = greeks(p, spec, cfg)
+        ref = np.array(c["greeks_price"])
+        assert abs(g["price"].estimate - ref.mean()) < 0.05
+        # fp32 and the reference consume the same Sobol points; only the
+        # inverse normal and arithmetic precision differ
+        np.testing.assert_allclose(g["price"].per_run_values, ref, rtol=2e-4)
+
+    def test_sobol_index_range_limit(self, params, euro_call):
+        cfg = SimConfig(scheme="milstein", sampler="sobol", sobol_highdim_ack=True, n_paths=2**29,
+                        n_steps=4, n_runs=3)
+        with pytest.raises(UnsupportedProduct):
+            price(params, euro_call, cfg)
