@@ -94,7 +94,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:  # noqa: BLE001
                 pass
-            time.sleep(0.05)
+            time.sleep(0.01)
 
     def __enter__(self):
         if self.nv:
@@ -138,9 +138,10 @@ def cpu_reference_pass(n_paths: int, workers: int) -> float:
     return time.perf_counter() - t0
 
 
-def cpu_baseline_block(n_paths: int = 2 ** 16) -> dict:
+def cpu_baseline_block(n_paths: int = 0) -> dict:
     import oracle
     workers = os.cpu_count() or 1
+    n_paths = n_paths or max(2 ** 16, 4 * 4096 * workers)
     kind = "reference" if oracle.ref_core() is not None else "port"
     if kind == "port":
         return {"value": None, "unit": UNIT, "cores": workers, "kind": "port",
@@ -162,7 +163,7 @@ def run_reference(args) -> None:
     if oracle.ref_core() is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
-    n = 2 ** 15
+    n = max(2 ** 15, 2 * 4096 * workers)   # >= 2 reference jobs per worker
     for _ in range(args.warmup):
         cpu_reference_pass(n, workers)
     times = [cpu_reference_pass(n, workers) for _ in range(args.steps)]
@@ -256,14 +257,14 @@ def run_b200(args) -> None:
     # out; step tables H2D and sums D2H inside every timed call)
     e2e_times = []
     g = None
-    for i in range(max(2, args.steps // 2) + 1):
+    for i in range(0 if args.no_e2e else max(2, args.steps // 2) + 1):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         g = greeks(p, spec, cfg)
         e2e_times.append(time.perf_counter() - t0)
-    e2e_s = sorted(e2e_times[1:])[len(e2e_times[1:]) // 2]
+    e2e_s = sorted(e2e_times[1:])[len(e2e_times[1:]) // 2] if e2e_times else float("nan")
     te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
@@ -298,7 +299,7 @@ def run_b200(args) -> None:
                     "d2h_bytes_per_step": d2h, "ms_per_call": e2e_s * 1000.0},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk,
-            "estimates": {q: [g[q].estimate, g[q].path_std_error] for q in g},
+            "estimates": {q: [g[q].estimate, g[q].path_std_error] for q in g} if g else None,
         }
         if world == 1 and not args.no_cpu:
             line["cpu_baseline"] = cpu_baseline_block()
@@ -314,6 +315,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the public-API e2e leg (profiling)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

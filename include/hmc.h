@@ -129,7 +129,7 @@ int hmc_greeks_chunks(const hmc_model* model, const hmc_product* product,
                       const hmc_sim* sim, double* d_chunks, void* d_work,
                       void* stream);
 
-/* Fixed-order (compensated, sequential) sum of chunk partials
+/* Fixed-shape (strided sequential + 512-way tree) fp64 sum of chunk partials
  * d_chunks[run][0..n_chunks)[HMC_NW] -> d_out[run][HMC_NW].  Chunks must be
  * in global path order; the result is then bit-identical for any split of
  * the path axis across calls / GPUs.  Asynchronous on `stream`. */
@@ -160,6 +160,11 @@ int hmc_discretised_batch_f64(const hmc_model* model, double s0, double T,
  * Gray-code sequence is x_d(n) = 2^-30 * XOR_{b : bit b of n^(n>>1)} v[b][d]. */
 int hmc_sobol_init_directions(const int64_t* poly, const int64_t* vinit,
                               int32_t dim, uint32_t* v_out);
+
+/* Device Philox4x32-10 (fixed key 0xA4093822, 0x299F31D0 -- the production
+ * stream's key) on n HOST counters ctr[n][4] -> out[n][4]; for known-answer
+ * tests of the exact device code path.  Synchronous. */
+int hmc_philox_check(const uint32_t* ctr, int32_t n, uint32_t* out, int32_t device);
 
 /* Key derivation of the reference RNG (rng.py:46-52), for hosts that
  * build key_run for hmc_discretised_batch_f64. */

@@ -44,27 +44,31 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, defines: dict | None = None,
+          lib: str = LIB, objdir: str = BUILD) -> str:
+    """Compile and link; ``defines`` (e.g. {"HMC_SINCOS_POLY": 1}) build a
+    kernel variant into ``lib`` / ``objdir`` (used by tools/kernel_variants.py)."""
+    os.makedirs(objdir, exist_ok=True)
+    dflags = [f"-D{k}={v}" for k, v in (defines or {}).items()]
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(ROOT, "include", "hmc.h"))
     objs = []
     for unit, extra in UNITS.items():
         src = os.path.join(CSRC, unit)
-        obj = os.path.join(BUILD, unit.replace(".cu", ".o"))
+        obj = os.path.join(objdir, unit.replace(".cu", ".o"))
         objs.append(obj)
         if force or _stale(obj, [src, __file__] + headers):
-            cmd = [nvcc(), *ARCH, *COMMON, *extra, "-c", src, "-o", obj]
+            cmd = [nvcc(), *ARCH, *COMMON, *dflags, *extra, "-c", src, "-o", obj]
             if verbose:
                 cmd += ["-Xptxas", "-v"]
                 print(" ".join(cmd), flush=True)
             subprocess.run(cmd, check=True)
-    if force or _stale(LIB, objs):
-        cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+    if force or _stale(lib, objs):
+        cmd = [nvcc(), *ARCH, "-shared", "-o", lib, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

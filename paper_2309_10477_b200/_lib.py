@@ -15,7 +15,8 @@ import threading
 
 from .errors import DeviceError, UnsupportedProduct, ValidationError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhmc.so")
+LIB_PATH = os.environ.get("HMC_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libhmc.so")
 
 # mirrors of include/hmc.h
 HMC_ABI_VERSION = 1
@@ -38,7 +39,7 @@ EXPORTS = (
     "hmc_abi_version", "hmc_last_error", "hmc_device_count",
     "hmc_chunks_in_slice", "hmc_workspace_bytes", "hmc_greeks_chunks",
     "hmc_reduce_chunks", "hmc_greeks", "hmc_discretised_batch_f64",
-    "hmc_sobol_init_directions", "hmc_root_key", "hmc_derive_key",
+    "hmc_sobol_init_directions", "hmc_root_key", "hmc_derive_key", "hmc_philox_check",
 )
 
 
@@ -87,6 +88,8 @@ def _declare(L: ctypes.CDLL) -> None:
                                                      pd, ctypes.POINTER(i64), i64, pd, i32]),
         "hmc_sobol_init_directions": (ctypes.c_int, [ctypes.POINTER(i64), ctypes.POINTER(i64),
                                                      i32, ctypes.POINTER(ctypes.c_uint32)]),
+        "hmc_philox_check": (ctypes.c_int, [ctypes.POINTER(ctypes.c_uint32), i32,
+                                             ctypes.POINTER(ctypes.c_uint32), i32]),
         "hmc_root_key": (u64, [u64]),
         "hmc_derive_key": (u64, [u64, u64]),
     }

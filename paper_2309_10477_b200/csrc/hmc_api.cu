@@ -61,16 +61,20 @@ int check_model(const hmc_model* m) {
     return HMC_OK;
 }
 
-// step table shared by every kernel: t_k = k*T/n_steps computed exactly as
-// _core.pyx:406 (int k promoted to double, times T, divided by n_steps)
-void build_steps(int n_steps, double T, double h_r, const unsigned char* fix, Prepared& P) {
+// step tables shared by every kernel: t_k = k*T/n_steps computed exactly as
+// _core.pyx:406 (int k promoted to double, times T, divided by n_steps);
+// the fp32 table holds the fixing weights (E_k, E_k t_k, E_k expm1(+-h t_k))
+// with E_k = S0 e^{r t_k}, zero on non-fixing steps.
+void build_steps(int n_steps, double T, double h_r, double s0, double r,
+                 const unsigned char* fix, Prepared& P) {
     P.st64.resize((size_t)n_steps + 1);
     P.st32.resize((size_t)n_steps + 1);
     for (int k = 0; k <= n_steps; ++k) {
         const double t = k * T / n_steps;
         StepD s{t, std::expm1(h_r * t), std::expm1(-h_r * t), fix[k] ? 1.0 : 0.0};
         P.st64[k] = s;
-        P.st32[k] = make_float4((float)s.t, (float)s.e1p, (float)s.e1m, (float)s.fix);
+        const double E = fix[k] ? s0 * std::exp(r * t) : 0.0;
+        P.st32[k] = make_float4((float)E, (float)(E * t), (float)(E * s.e1p), (float)(E * s.e1m));
     }
 }
 
@@ -82,13 +86,29 @@ void fill_fp32_constants(KernelArgs& a) {
     a.f_cmil = (float)(mil * 0.25 * a.sigma * a.sigma);
     a.f_sigma = (float)a.sigma;
     a.f_nhdt2 = (float)(-0.5 * a.dt * log2e);
-    a.f_bm = (float)(-2.0 * ln2 * a.dt);
-    a.f_rl2 = (float)(a.r * log2e);
-    a.f_l2s0 = (float)std::log2(a.s0);
+    a.f_bm2 = (float)(-2.0 * ln2 * a.dt * log2e * log2e);
+    a.f_cA = (float)(a.sigma * a.rho / log2e);
+    a.f_cB = (float)(a.sigma * a.sq1mr2 / log2e);
+    a.f_cmil2 = (float)(0.25 * mil);
     a.f_log2e = (float)log2e;
     a.f_rho = (float)a.rho;
     a.f_sq1mr2 = (float)a.sq1mr2;
     a.f_sqdt = (float)std::sqrt(a.dt);
+    a.f_v0 = (float)a.v0;
+    a.f_vu = (float)a.v0_up;
+    a.f_vd = (float)a.v0_dn;
+    a.f_K = (float)a.K;
+    a.f_T = (float)a.T;
+    a.f_disc = (float)a.disc;
+    a.f_disc_up = (float)a.disc_up;
+    a.f_disc_dn = (float)a.disc_dn;
+    a.f_inv_s0 = (float)(1.0 / a.s0);
+    a.f_up_ratio = (float)((a.s0 + a.h_spot) / a.s0);
+    a.f_dn_ratio = (float)((a.s0 - a.h_spot) / a.s0);
+    a.f_inv_2h = a.h_spot > 0.0 ? (float)(0.5 / a.h_spot) : 0.0f;
+    a.f_inv_dv = a.v0_up > a.v0_dn ? (float)(1.0 / (a.v0_up - a.v0_dn)) : 0.0f;
+    a.f_inv_2hr = a.h_r > 0.0 ? (float)(0.5 / a.h_r) : 0.0f;
+    a.f_inv_navg = (float)(1.0 / a.n_avg);
 }
 
 int prepare(const hmc_model* m, const hmc_product* pr, const hmc_sim* sim, Prepared& P) {
@@ -126,6 +146,9 @@ int prepare(const hmc_model* m, const hmc_product* pr, const hmc_sim* sim, Prepa
         if (!(sim->v0_up > sim->v0_dn && sim->v0_dn >= 0.0)) return fail(HMC_E_INVALID, "need v0_up > v0_dn >= 0");
         if (!(sim->h_r > 0.0)) return fail(HMC_E_INVALID, "need h_r > 0");
     }
+    if (sim->sampler == HMC_SAMPLER_PSEUDO && sim->precision == HMC_PREC_FP32 &&
+        sim->n_paths > 4294967296LL)
+        return fail(HMC_E_INVALID, "the Philox counter addresses at most 2^32 paths per run");
     if (sim->sampler == HMC_SAMPLER_SOBOL) {
         if (!sim->sobol_v) return fail(HMC_E_INVALID, "sobol sampler needs direction numbers");
         if (1.0 + (double)sim->n_runs * (double)sim->n_paths > 1073741824.0)
@@ -160,17 +183,12 @@ int prepare(const hmc_model* m, const hmc_product* pr, const hmc_sim* sim, Prepa
     a.path_lo = sim->path_lo;
     a.path_hi = sim->path_hi;
     a.root_key = hmc_root_key(sim->seed);
-    const uint32_t k0 = (uint32_t)a.root_key, k1 = (uint32_t)(a.root_key >> 32);
-    for (int i = 0; i < 10; ++i) {
-        a.rk0[i] = k0 + (uint32_t)i * 0x9E3779B9u;
-        a.rk1[i] = k1 + (uint32_t)i * 0xBB67AE85u;
-    }
     a.sobol_dim = 2 * sim->n_steps;
-    fill_fp32_constants(a);
 
+    fill_fp32_constants(a);
     std::vector<unsigned char> fix((size_t)sim->n_steps + 1, 0);
     for (long long i = 0; i < pr->n_avg; ++i) fix[pr->avg_idx[i]] = 1;
-    build_steps(sim->n_steps, pr->maturity, a.h_r, fix.data(), P);
+    build_steps(sim->n_steps, pr->maturity, a.h_r, pr->spot, m->r, fix.data(), P);
 
     const long long n = sim->path_hi - sim->path_lo;
     P.n_tiles = n_tiles_of(n);
@@ -205,24 +223,35 @@ __global__ void tiles_to_chunks_kernel(const double* __restrict__ tiles, long lo
     chunks[((size_t)run * n_chunks + c) * kNW + w] = s;
 }
 
-// Neumaier-compensated sequential sum over chunks in global path order
-__global__ void chunks_to_runs_kernel(const double* __restrict__ chunks, long long n_chunks,
-                                      double* __restrict__ out) {
-    const int w = threadIdx.x;
-    if (w >= kNW) return;
+// Sum over chunks in global path order with a FIXED shape: thread t owns
+// chunks t, t + 512, ... (sequential), then a fixed 512-way tree.  The shape
+// depends only on the global chunk count, never on how the chunks were
+// produced, so 1 GPU and N GPUs give bit-identical results.
+constexpr int kRunThreads = 512;
+
+__global__ void __launch_bounds__(kRunThreads) chunks_to_runs_kernel(const double* __restrict__ chunks,
+                                                                    long long n_chunks,
+                                                                    double* __restrict__ out) {
+    __shared__ double red[kRunThreads];
     const int run = blockIdx.x;
     const double* src = chunks + (size_t)run * n_chunks * kNW;
-    double s = 0.0, c = 0.0;
-    for (long long i = 0; i < n_chunks; ++i) {
-        const double x = src[i * kNW + w];
-        const double t = s + x;
-        if (fabs(s) >= fabs(x))
-            c += (s - t) + x;
-        else
-            c += (x - t) + s;
-        s = t;
+    double acc[kNW];
+#pragma unroll
+    for (int w = 0; w < kNW; ++w) acc[w] = 0.0;
+    for (long long c = threadIdx.x; c < n_chunks; c += kRunThreads) {
+#pragma unroll
+        for (int w = 0; w < kNW; ++w) acc[w] += src[c * kNW + w];
     }
-    out[(size_t)run * kNW + w] = s + c;
+    for (int w = 0; w < kNW; ++w) {
+        red[threadIdx.x] = acc[w];
+        __syncthreads();
+        for (int s = kRunThreads / 2; s > 0; s >>= 1) {
+            if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) out[(size_t)run * kNW + w] = red[0];
+        __syncthreads();
+    }
 }
 
 cudaError_t launch_tiles_to_chunks(const double* d_tiles, long long n_tiles, int n_runs,
@@ -232,9 +261,17 @@ cudaError_t launch_tiles_to_chunks(const double* d_tiles, long long n_tiles, int
     return cudaGetLastError();
 }
 
+__global__ void philox_kat_kernel(const uint4* __restrict__ ctr, uint4* __restrict__ out, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        const uint4 c = ctr[i];
+        out[i] = philox4x32_10(c.x, c.y, c.z, c.w);
+    }
+}
+
 cudaError_t launch_chunks_to_runs(const double* d_chunks, long long n_chunks, int n_runs,
                                   double* d_out, cudaStream_t s) {
-    chunks_to_runs_kernel<<<(unsigned)n_runs, 32, 0, s>>>(d_chunks, n_chunks, d_out);
+    chunks_to_runs_kernel<<<(unsigned)n_runs, kRunThreads, 0, s>>>(d_chunks, n_chunks, d_out);
     return cudaGetLastError();
 }
 
@@ -387,7 +424,7 @@ int hmc_discretised_batch_f64(const hmc_model* model, double s0, double T, int32
     a.path_hi = path_hi;
     std::vector<unsigned char> fix((size_t)n_steps + 1, 0);
     for (int64_t i = 0; i < n_avg; ++i) fix[avg_idx[i]] = 1;
-    build_steps(n_steps, T, 0.0, fix.data(), P);
+    build_steps(n_steps, T, 0.0, s0, model->r, fix.data(), P);
 
     HMC_CK(cudaSetDevice(device));
     cudaStream_t s;
@@ -413,6 +450,24 @@ int hmc_discretised_batch_f64(const hmc_model* model, double s0, double T, int32
     cudaStreamDestroy(s);
     HMC_CK(e);
     HMC_CK(e2);
+    return HMC_OK;
+}
+
+int hmc_philox_check(const uint32_t* ctr, int32_t n, uint32_t* out, int32_t device) {
+    if (!ctr || !out || n < 1) return fail(HMC_E_INVALID, "bad philox check arguments");
+    HMC_CK(cudaSetDevice(device));
+    uint4 *d_c = nullptr, *d_o = nullptr;
+    HMC_CK(cudaMalloc((void**)&d_c, (size_t)n * sizeof(uint4)));
+    cudaError_t e = cudaMalloc((void**)&d_o, (size_t)n * sizeof(uint4));
+    if (e == cudaSuccess) e = cudaMemcpy(d_c, ctr, (size_t)n * sizeof(uint4), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        hmc::philox_kat_kernel<<<(n + 127) / 128, 128>>>(d_c, d_o, n);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(out, d_o, (size_t)n * sizeof(uint4), cudaMemcpyDeviceToHost);
+    cudaFree(d_c);
+    cudaFree(d_o);
+    HMC_CK(e);
     return HMC_OK;
 }
 

@@ -48,12 +48,12 @@ struct KernelArgs {
     int sampler;
     int n_runs;
     long long n_paths, path_lo, path_hi;
-    // pseudo: Philox round keys (fp32 path) / SplitMix64 root key (fp64 path)
-    uint32_t rk0[10], rk1[10];
+    // root_key(seed) (rng.py:46-47): per-run stream key derivation for both
+    // the Philox counter (fp32) and the SplitMix64 stream (fp64)
     unsigned long long root_key;
     // tables (device pointers)
     const StepD* steps64;       // [n_steps + 1]
-    const float4* steps32;      // [n_steps + 1]
+    const float4* steps32;      // [n_steps + 1] fixing weights, see FixW
     const uint32_t* sobol_v;    // [30][sobol_dim]
     int sobol_dim;
     // fp32 derived constants (host-computed in fp64, rounded once)
@@ -62,30 +62,56 @@ struct KernelArgs {
     float f_cmil;    // milstein * sigma^2 / 4
     float f_sigma;
     float f_nhdt2;   // -0.5 dt log2(e)
-    float f_bm;      // -2 ln(2) dt     (Box-Muller radius^2 per lg2 unit)
-    float f_rl2;     // r log2(e)
-    float f_l2s0;    // log2(S0)
+    float f_bm2;     // -2 ln(2) dt log2(e)^2: R' = sqrt(f_bm2 lg2 u1) = sqrt(dt) |z| log2 e
+    float f_cA;      // sigma rho / log2(e)
+    float f_cB;      // sigma sqrt(1 - rho^2) / log2(e)
+    float f_cmil2;   // milstein / 4  (multiplies (sigma sqrt(dt) z2)^2)
     float f_log2e;
     float f_rho, f_sq1mr2;
     float f_sqdt;    // sqrt(dt)
+    // fp32 epilogue constants (no double->float conversions or divisions on
+    // the device: F2F and MUFU.RCP share the MIO queue with the path MUFUs)
+    float f_v0, f_vu, f_vd;
+    float f_K, f_T, f_disc, f_disc_up, f_disc_dn;
+    float f_inv_s0, f_up_ratio, f_dn_ratio;   // 1/S0, (S0 +- h)/S0
+    float f_inv_2h, f_inv_dv, f_inv_2hr;      // 1/(2 h_S), 1/(v0u - v0d), 1/(2 h_r)
+    float f_inv_navg;
 };
 
+// fp32 fixing weights of step k (host-computed in fp64):
+//   x = E_k = S0 e^{r t_k},  y = E_k t_k,  z = E_k expm1(h_r t_k),
+//   w = E_k expm1(-h_r t_k);  all zero when k is not a fixing date.
+// With P = 2^{L_k} (L = r-free log2 price ratio), S_k = P E_k.
+
 // ---------------------------------------------------------------------------
-// Philox4x32-10 (Salmon et al., SC'11).  Counter = (step pair, path lo, path
-// hi, run); key = root_key(seed) so the 10 round keys are kernel parameters
-// (constant-bank operands, no registers).
+// Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11) with a fixed key: the
+// round keys are compile-time immediates of the LOP3s (no constant loads in
+// the step loop).  Streams are separated through the counter instead:
+//   (c0, c1, c2, c3) = (step pair, path, lo32, hi32 of key_run),
+//   key_run = derive(root_key(seed), run)  -- the reference's per-run key
+//   derivation (engine.py:96, rng.py:46-52), 64 bits of stream id.
 // ---------------------------------------------------------------------------
+constexpr uint32_t kPhiloxK0 = 0xA4093822u, kPhiloxK1 = 0x299F31D0u;
+
+// 32x32 -> 64 multiply as ONE IMAD.WIDE.U32 (the plain C++ form makes ptxas
+// add a zero high word after every multiply)
+__device__ __forceinline__ void mulhilo32(uint32_t a, uint32_t b, uint32_t& hi, uint32_t& lo) {
+    asm("{\n\t.reg .b64 t;\n\tmul.wide.u32 t, %2, %3;\n\tmov.b64 {%1, %0}, t;\n\t}"
+        : "=r"(hi), "=r"(lo) : "r"(a), "r"(b));
+}
+
 __device__ __forceinline__ uint4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2,
-                                               uint32_t c3, const KernelArgs& a) {
+                                               uint32_t c3) {
 #pragma unroll
     for (int i = 0; i < 10; ++i) {
-        const unsigned long long p0 = (unsigned long long)0xD2511F53u * c0;
-        const unsigned long long p1 = (unsigned long long)0xCD9E8D57u * c2;
-        const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
-        const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
-        c0 = hi1 ^ c1 ^ a.rk0[i];
+        const uint32_t k0 = kPhiloxK0 + (uint32_t)i * 0x9E3779B9u;
+        const uint32_t k1 = kPhiloxK1 + (uint32_t)i * 0xBB67AE85u;
+        uint32_t hi0, lo0, hi1, lo1;
+        mulhilo32(0xD2511F53u, c0, hi0, lo0);
+        mulhilo32(0xCD9E8D57u, c2, hi1, lo1);
+        c0 = hi1 ^ c1 ^ k0;
         c1 = lo1;
-        c2 = hi0 ^ c3 ^ a.rk1[i];
+        c2 = hi0 ^ c3 ^ k1;
         c3 = lo0;
     }
     return make_uint4(c0, c1, c2, c3);
@@ -194,6 +220,28 @@ __device__ __forceinline__ void greeks_epilogue(const KernelArgs& a, T A, T tw, 
     q[HMC_Q_VEGA] = (double)((payoff(Au, disc) - payoff(Ad, disc)) / (T)(a.v0_up - a.v0_dn));
     q[HMC_Q_RHO_FD] = (double)((payoff(Rp, (T)a.disc_up) - payoff(Rm, (T)a.disc_dn)) /
                                (T(2) * (T)a.h_r));
+}
+
+// fp32 twin of greeks_epilogue: same estimators, host-precomputed
+// reciprocals instead of divisions
+__device__ __forceinline__ void greeks_epilogue_f32(const KernelArgs& a, float A, float tw, float Au,
+                                                    float Ad, float Rp, float Rm, double (&q)[kNQ]) {
+    const float K = a.f_K, disc = a.f_disc;
+    auto payoff = [&](float x, float d) -> float {
+        return a.is_call ? d * pos_part(x - K) : d * pos_part(K - x);
+    };
+    q[HMC_Q_PRICE] = (double)payoff(A, disc);
+    const float dA = disc * A * a.f_inv_s0;
+    const bool itm = A > K;
+    q[HMC_Q_DELTA] = itm ? (double)dA : 0.0;
+    q[HMC_Q_RHO] = itm ? (a.is_asian ? (double)(disc * (tw - a.f_T * (A - K))) : (double)(disc * K * a.f_T))
+                       : 0.0;
+    const float Aup = A * a.f_up_ratio, Adn = A * a.f_dn_ratio;
+    const float ind = (float)((Aup > K) ? 1 : 0) - (float)((Adn > K) ? 1 : 0);
+    q[HMC_Q_GAMMA] = (double)(ind * dA * a.f_inv_2h);
+    q[HMC_Q_DELTA_FD] = (double)((payoff(Aup, disc) - payoff(Adn, disc)) * a.f_inv_2h);
+    q[HMC_Q_VEGA] = (double)((payoff(Au, disc) - payoff(Ad, disc)) * a.f_inv_dv);
+    q[HMC_Q_RHO_FD] = (double)((payoff(Rp, a.f_disc_up) - payoff(Rm, a.f_disc_dn)) * a.f_inv_2hr);
 }
 
 }  // namespace hmc

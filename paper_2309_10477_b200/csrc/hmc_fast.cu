@@ -4,8 +4,8 @@
 // time steps, nothing but the final fp64 tile partials touches HBM:
 //
 //   per path:  3 variance trajectories (v0, v0 + h, v0 - h) driven by the
-//              same normals (common random numbers); log-price of each in
-//              log2 units; running fixing sums; for the base trajectory also
+//              same normals (common random numbers); r-free log2 price ratio
+//              L of each; running fixing sums; for the base trajectory also
 //              sum S t (Asian pathwise Rho) and sum S expm1(+-h t) (r bumps)
 //   per step:  2 correlated normals -- Box-Muller on Philox4x32-10 (pseudo)
 //              or Giles' erfinv on an on-the-fly Gray-code Sobol point (QMC)
@@ -13,17 +13,30 @@
 //              algebraically regrouped so the step-shared terms are computed
 //              once per thread, not once per trajectory:
 //                v' = max(v (1 - k dt) + c_k + (sigma sqrt(dt) z2) sqrt(v), 0)
-//                c_k = k theta dt + sigma^2/4 (dt z2^2 - dt)      (Milstein)
+//                c_k = k theta dt + sigma^2/4 ((sqrt(dt) z2)^2 - dt)  (Milstein)
 //                L' = L + sqrt(v) (sqrt(dt) z1 log2 e) - v dt/2 log2 e
-//              S_k = 2^(L_k + log2 S0 + r t_k log2 e) only at fixing dates
+//              S_k = E_k 2^{L_k}, E_k = S0 e^{r t_k}, only at fixing dates
 //
-// Bound: the MUFU (XU) pipe -- per Asian daily-fixing step 4 (lg2, sqrt,
-// sin, cos) + 3 x (sqrt, ex2) = 10 MUFU ops vs ~70 other issue slots
-// (DESIGN.md "roofline").
+// The loop is bound jointly by instruction issue and the MUFU (XU) pipe
+// (DESIGN.md "roofline").  Build-time switches trade MUFU ops for FMA-pipe
+// polynomials:
+//   HMC_SINCOS_POLY  Box-Muller angle via sin/cos polynomials (-2 MUFU/step)
+//   HMC_EX2_POLY     number of trajectories (0..3) whose 2^L uses a
+//                    polynomial instead of MUFU.EX2 (-1 MUFU/step each)
 #include <cuda_runtime.h>
 
 #include "hmc_device.cuh"
 #include "hmc_launch.h"
+
+#ifndef HMC_SINCOS_POLY
+#define HMC_SINCOS_POLY 0
+#endif
+#ifndef HMC_EX2_POLY
+#define HMC_EX2_POLY 0
+#endif
+#ifndef HMC_SQRT_RSQ
+#define HMC_SQRT_RSQ 0
+#endif
 
 namespace hmc {
 
@@ -42,22 +55,82 @@ __device__ __forceinline__ float sqrta(float x) {
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
-
-// uniform in [1, 2) from 23 random bits (no int->float conversion on the XU pipe)
-__device__ __forceinline__ float one_to_two(uint32_t x) {
-    return __uint_as_float((x & 0x007fffffu) | 0x3f800000u);
+__device__ __forceinline__ float rsqrta(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// sqrt(v) of a variance (v >= 0): MUFU.SQRT, or v * MUFU.RSQ(v) (exact 0 at v = 0)
+__device__ __forceinline__ float sqrt_var(float v) {
+#if HMC_SQRT_RSQ
+    return v * rsqrta(fmaxf(v, 1e-30f));
+#else
+    return sqrta(v);
+#endif
 }
 
-// Box-Muller: radius from xr, angle from xa; returns the step shocks
-//   z1l = sqrt(dt) z1 log2(e),   z2s = sqrt(dt) (rho z1 + sqrt(1-rho^2) zb)
+// 2^x on the FMA pipe: x = j + f, |f| <= 1/2, 2^f by a degree-6 Taylor
+// polynomial (rel. err 1.6e-7), exponent added with one LEA.
+__device__ __forceinline__ float ex2_poly(float x) {
+    const float magic = 12582912.0f;  // 1.5 * 2^23: rounds to integer
+    x = fmaxf(x, -125.0f);            // keep the exponent add in range
+    const float m = x + magic;
+    const float f = x - (m - magic);
+    float p = 1.5403530393381606e-4f;
+    p = fmaf(p, f, 1.3333558146428441e-3f);
+    p = fmaf(p, f, 9.6181291076284772e-3f);
+    p = fmaf(p, f, 5.5504108664821576e-2f);
+    p = fmaf(p, f, 2.4022650695910071e-1f);
+    p = fmaf(p, f, 6.9314718055994531e-1f);
+    p = fmaf(p, f, 1.0f);
+    return __uint_as_float(__float_as_uint(p) + (__float_as_uint(m) << 23));
+}
+
+template <int POLY>
+__device__ __forceinline__ float ex2_sel(float x) {
+    if (POLY) return ex2_poly(x);
+    return ex2a(x);
+}
+
+// uniform in [1, 2) from the top 23 bits of x: one LEA.HI
+__device__ __forceinline__ float one_to_two(uint32_t x) {
+    return __uint_as_float((x >> 9) + 0x3f800000u);
+}
+
+// Box-Muller on two Philox words; returns the step shocks
+//   z1l = sqrt(dt) z1 log2(e),   sz2 = sigma sqrt(dt) (rho z1 + sqrt(1-rho^2) zb)
 __device__ __forceinline__ void box_muller(uint32_t xr, uint32_t xa, const KernelArgs& a,
-                                           float& z1l, float& z2s) {
-    const float u1 = 2.0f - one_to_two(xr);                 // (0, 1]
-    const float R = sqrta(lg2a(u1) * a.f_bm);               // sqrt(dt) sqrt(-2 ln u1)
+                                           float& z1l, float& sz2) {
+    const float u1 = 2.0f - one_to_two(xr);                  // (0, 1]
+    const float R = sqrta(lg2a(u1) * a.f_bm2);               // sqrt(dt) sqrt(-2 ln u1) log2 e
+    float sn, cs;
+#if HMC_SINCOS_POLY
+    // angle in [-pi/2, pi/2) from the top 23 bits, sin/cos by Taylor
+    // polynomials (abs err 6e-8), cos sign from a spare (low) bit of xr
+    const float r = fmaf(one_to_two(xa), 2.0f, -3.0f);       // [-1, 1)
+    const float r2 = r * r;
+    float ps = -3.598843235212084e-06f;
+    ps = fmaf(ps, r2, 1.6044118478735975e-04f);
+    ps = fmaf(ps, r2, -4.681754135318687e-03f);
+    ps = fmaf(ps, r2, 7.969262624616703e-02f);
+    ps = fmaf(ps, r2, -6.459640975062462e-01f);
+    ps = fmaf(ps, r2, 1.5707963267948966f);
+    sn = ps * r;
+    float pc = 4.710874778818169e-07f;
+    pc = fmaf(pc, r2, -2.5202042373060596e-05f);
+    pc = fmaf(pc, r2, 9.192602748394263e-04f);
+    pc = fmaf(pc, r2, -2.0863480763352957e-02f);
+    pc = fmaf(pc, r2, 2.53669507901048e-01f);
+    pc = fmaf(pc, r2, -1.2337005501361697f);
+    pc = fmaf(pc, r2, 1.0f);
+    cs = __uint_as_float(__float_as_uint(pc) ^ (xr << 31));
+#else
     const float th = fmaf(one_to_two(xa), 6.28318530717958647692f, -9.42477796076937971538f);
-    const float sn = __sinf(th), cs = __cosf(th);           // th in [-pi, pi)
-    z1l = (R * a.f_log2e) * cs;
-    z2s = fmaf(R * a.f_rho, cs, (R * a.f_sq1mr2) * sn);
+    sn = __sinf(th);                                         // th in [-pi, pi)
+    cs = __cosf(th);
+#endif
+    z1l = R * cs;
+    sz2 = R * fmaf(a.f_cA, cs, a.f_cB * sn);
 }
 
 // Standard-normal quantile of the Sobol coordinate x * 2^-30 (x in [1, 2^30)):
@@ -103,49 +176,46 @@ struct PathState32 {
     float T1, Dp, Dm;  // base: sum S t, sum S expm1(h t), sum S expm1(-h t)
 };
 
-template <bool GREEKS>
 __device__ __forceinline__ void traj_step(float& v, float& L, float z1l, float sz2, float ck,
                                           const KernelArgs& a) {
-    const float s = sqrta(v);
+    const float s = sqrt_var(v);
     L = fmaf(s, z1l, L);
     L = fmaf(v, a.f_nhdt2, L);
     v = fmaxf(fmaf(s, sz2, fmaf(v, a.f_omkdt, ck)), 0.0f);
 }
 
 template <bool GREEKS>
-__device__ __forceinline__ void advance(PathState32& st, float z1l, float z2s, const KernelArgs& a) {
-    const float sz2 = a.f_sigma * z2s;
-    const float ck = fmaf(z2s * z2s, a.f_cmil, a.f_ck0);
-    traj_step<GREEKS>(st.v0, st.L0, z1l, sz2, ck, a);
+__device__ __forceinline__ void advance(PathState32& st, float z1l, float sz2, const KernelArgs& a) {
+    const float ck = fmaf(sz2 * sz2, a.f_cmil2, a.f_ck0);
+    traj_step(st.v0, st.L0, z1l, sz2, ck, a);
     if (GREEKS) {
-        traj_step<GREEKS>(st.vu, st.Lu, z1l, sz2, ck, a);
-        traj_step<GREEKS>(st.vd, st.Ld, z1l, sz2, ck, a);
+        traj_step(st.vu, st.Lu, z1l, sz2, ck, a);
+        traj_step(st.vd, st.Ld, z1l, sz2, ck, a);
     }
 }
 
 template <bool GREEKS>
-__device__ __forceinline__ void fixing(PathState32& st, const float4 tab, const KernelArgs& a) {
-    const float rt2 = fmaf(tab.x, a.f_rl2, a.f_l2s0);
-    const float S = ex2a(st.L0 + rt2);
-    st.A0 += S;
+__device__ __forceinline__ void fixing(PathState32& st, const float4 w) {
+    const float P = ex2_sel<(HMC_EX2_POLY >= 3)>(st.L0);
+    st.A0 = fmaf(P, w.x, st.A0);
     if (GREEKS) {
-        st.T1 = fmaf(S, tab.x, st.T1);
-        st.Dp = fmaf(S, tab.y, st.Dp);
-        st.Dm = fmaf(S, tab.z, st.Dm);
-        st.Au += ex2a(st.Lu + rt2);
-        st.Ad += ex2a(st.Ld + rt2);
+        st.T1 = fmaf(P, w.y, st.T1);
+        st.Dp = fmaf(P, w.z, st.Dp);
+        st.Dm = fmaf(P, w.w, st.Dm);
+        st.Au = fmaf(ex2_sel<(HMC_EX2_POLY >= 1)>(st.Lu), w.x, st.Au);
+        st.Ad = fmaf(ex2_sel<(HMC_EX2_POLY >= 2)>(st.Ld), w.x, st.Ad);
     }
 }
 
 template <int FIX, bool GREEKS>
-__device__ __forceinline__ void step(PathState32& st, int k, float z1l, float z2s,
+__device__ __forceinline__ void step(PathState32& st, int k, float z1l, float sz2,
                                      const KernelArgs& a) {
-    advance<GREEKS>(st, z1l, z2s, a);
+    advance<GREEKS>(st, z1l, sz2, a);
     if (FIX == kFixEvery) {
-        fixing<GREEKS>(st, __ldg(a.steps32 + k), a);
+        fixing<GREEKS>(st, __ldg(a.steps32 + k));
     } else if (FIX == kFixTable) {
-        const float4 tab = __ldg(a.steps32 + k);
-        if (tab.w != 0.0f) fixing<GREEKS>(st, tab, a);
+        const float4 w = __ldg(a.steps32 + k);
+        if (w.x != 0.0f) fixing<GREEKS>(st, w);
     }
 }
 
@@ -159,59 +229,61 @@ __global__ void __launch_bounds__(kTile) fast_greeks_kernel(const KernelArgs a,
     const long long p = live ? path : a.path_lo;
 
     PathState32 st;
-    st.v0 = (float)a.v0;
-    st.vu = (float)a.v0_up;
-    st.vd = (float)a.v0_dn;
+    st.v0 = a.f_v0;
+    st.vu = a.f_vu;
+    st.vd = a.f_vd;
     st.L0 = st.Lu = st.Ld = 0.0f;
     st.A0 = st.Au = st.Ad = 0.0f;
     st.T1 = st.Dp = st.Dm = 0.0f;
 
     if (SAMPLER == HMC_SAMPLER_PSEUDO) {
-        // Philox counter (pair j, path lo, path hi, run); key = root_key(seed)
-        const uint32_t c1 = (uint32_t)p, c2 = (uint32_t)((unsigned long long)p >> 32);
-        const uint32_t c3 = (uint32_t)run;
+        // counter (step pair, path, key_run lo, key_run hi), fixed key
+        const unsigned long long key_run = derive(a.root_key, (unsigned long long)run);
+        const uint32_t c1 = (uint32_t)p;
+        const uint32_t c2 = (uint32_t)key_run, c3 = (uint32_t)(key_run >> 32);
         const int npairs = a.n_sim >> 1;
         int k = 1;
 #pragma unroll 1
         for (int j = 0; j < npairs; ++j) {
-            const uint4 x = philox4x32_10((uint32_t)j, c1, c2, c3, a);
-            float z1l, z2s;
-            box_muller(x.x, x.y, a, z1l, z2s);
-            step<FIX, GREEKS>(st, k, z1l, z2s, a);
-            box_muller(x.z, x.w, a, z1l, z2s);
-            step<FIX, GREEKS>(st, k + 1, z1l, z2s, a);
+            const uint4 x = philox4x32_10((uint32_t)j, c1, c2, c3);
+            float z1l, sz2;
+            box_muller(x.x, x.y, a, z1l, sz2);
+            step<FIX, GREEKS>(st, k, z1l, sz2, a);
+            box_muller(x.z, x.w, a, z1l, sz2);
+            step<FIX, GREEKS>(st, k + 1, z1l, sz2, a);
             k += 2;
         }
         if (a.n_sim & 1) {
-            const uint4 x = philox4x32_10((uint32_t)npairs, c1, c2, c3, a);
-            float z1l, z2s;
-            box_muller(x.x, x.y, a, z1l, z2s);
-            step<FIX, GREEKS>(st, k, z1l, z2s, a);
+            const uint4 x = philox4x32_10((uint32_t)npairs, c1, c2, c3);
+            float z1l, sz2;
+            box_muller(x.x, x.y, a, z1l, sz2);
+            step<FIX, GREEKS>(st, k, z1l, sz2, a);
         }
     } else {
         // engine.py:100: run r uses Sobol rows 1 + r*n_paths + path
         const uint32_t n = (uint32_t)(1 + (long long)run * a.n_paths + p);
         const uint32_t gray = n ^ (n >> 1);
         const float c1 = a.f_sqdt * a.f_log2e;
+        const float cs = a.f_sigma * a.f_sqdt;
 #pragma unroll 1
         for (int k = 1; k <= a.n_sim; ++k) {
             const float za = sobol_normal(sobol_coord(gray, a.sobol_v, a.sobol_dim, 2 * (k - 1)));
             const float zb = sobol_normal(sobol_coord(gray, a.sobol_v, a.sobol_dim, 2 * k - 1));
             const float z1l = c1 * za;
-            const float z2s = a.f_sqdt * fmaf(a.f_rho, za, a.f_sq1mr2 * zb);
-            step<FIX, GREEKS>(st, k, z1l, z2s, a);
+            const float sz2 = cs * fmaf(a.f_rho, za, a.f_sq1mr2 * zb);
+            step<FIX, GREEKS>(st, k, z1l, sz2, a);
         }
     }
-    if (FIX == kFixLast) fixing<GREEKS>(st, __ldg(a.steps32 + a.n_sim), a);
+    if (FIX == kFixLast) fixing<GREEKS>(st, __ldg(a.steps32 + a.n_sim));
 
-    const float inv_n = 1.0f / (float)a.n_avg;
+    const float inv_n = a.f_inv_navg;
     const float A = st.A0 * inv_n;
     double q[kNQ];
     if (GREEKS) {
-        greeks_epilogue<float>(a, A, st.T1 * inv_n, st.Au * inv_n, st.Ad * inv_n,
-                               fmaf(st.Dp, inv_n, A), fmaf(st.Dm, inv_n, A), q);
+        greeks_epilogue_f32(a, A, st.T1 * inv_n, st.Au * inv_n, st.Ad * inv_n,
+                            fmaf(st.Dp, inv_n, A), fmaf(st.Dm, inv_n, A), q);
     } else {
-        const float K = (float)a.K, disc = (float)a.disc;
+        const float K = a.f_K, disc = a.f_disc;
         q[0] = (double)(a.is_call ? disc * pos_part(A - K) : disc * pos_part(K - A));
 #pragma unroll
         for (int i = 1; i < kNQ; ++i) q[i] = 0.0;

@@ -1,0 +1,89 @@
+#!/usr/bin/env python
+"""Build / time build-time variants of the production kernel (dev tool).
+
+    python tools/kernel_variants.py build          # here (nvcc, no GPU)
+    python tools/kernel_variants.py time [K]       # on the GPU box
+
+Each variant is a full libhmc.so built with different HMC_* switches into
+paper_2309_10477_b200/_variants/ and timed in a fresh process (HMC_LIB_PATH)
+on the bench workload (2^24-path Asian daily-fixing full Greeks).
+"""
+
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+VDIR = os.path.join(ROOT, "paper_2309_10477_b200", "_variants")
+
+VARIANTS = {
+    "base": {},
+    "rsq": {"HMC_SQRT_RSQ": 1},
+    "sincos": {"HMC_SINCOS_POLY": 1},
+    "ex2x1": {"HMC_EX2_POLY": 1},
+    "rsq_ex2x1": {"HMC_SQRT_RSQ": 1, "HMC_EX2_POLY": 1},
+}
+
+
+def build():
+    from paper_2309_10477_b200 import _build
+    os.makedirs(VDIR, exist_ok=True)
+    for name, d in VARIANTS.items():
+        lib = os.path.join(VDIR, f"libhmc_{name}.so")
+        _build.build(defines=d, lib=lib, objdir=os.path.join(VDIR, f"obj_{name}"))
+        sass = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True).stdout
+        print(name, lib, "MUFU:", sass.count("MUFU."))
+
+
+CHILD = r"""
+import ctypes, json, sys, time
+import torch
+sys.path.insert(0, %(root)r)
+from paper_2309_10477_b200 import _lib, engine, greeks
+import bench
+p, spec, cfg = bench.workload()
+job = engine.Job(p, spec, cfg, True)
+L = _lib.lib()
+work = torch.empty(L.hmc_workspace_bytes(ctypes.byref(job.sim)), dtype=torch.uint8, device="cuda")
+loc = torch.zeros((1, -(-cfg.n_paths // 16384), 14), dtype=torch.float64, device="cuda")
+def run():
+    _lib.check(L.hmc_greeks_chunks(ctypes.byref(job.model), ctypes.byref(job.product), ctypes.byref(job.sim),
+        ctypes.c_void_p(loc.data_ptr()), ctypes.c_void_p(work.data_ptr()), None))
+for _ in range(3): run()
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+ts = []
+for _ in range(%(k)d):
+    e0.record(); run(); e1.record(); torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
+g = greeks(p, spec, cfg)
+print(json.dumps({"ms": sorted(ts)[len(ts)//2], "min": min(ts),
+                  "est": {q: [g[q].estimate, g[q].path_std_error] for q in ("price","delta","gamma","vega","rho")}}))
+"""
+
+
+def time_all(k=10):
+    out = {}
+    for name in VARIANTS:
+        lib = os.path.join(VDIR, f"libhmc_{name}.so")
+        env = dict(os.environ, HMC_LIB_PATH=lib)
+        r = subprocess.run([sys.executable, "-c", CHILD % {"root": ROOT, "k": k}], env=env,
+                           capture_output=True, text=True, cwd=ROOT)
+        line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-2000:]
+        print(name, line, flush=True)
+        try:
+            out[name] = json.loads(line)
+        except Exception:
+            out[name] = {"error": line}
+    return out
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "build":
+        build()
+    else:
+        res = time_all(int(sys.argv[2]) if len(sys.argv) > 2 else 10)
+        os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+        with open(os.path.join(ROOT, "gpurun_out", "variants.json"), "w") as f:
+            json.dump(res, f, indent=1)
