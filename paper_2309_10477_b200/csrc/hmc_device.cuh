@@ -100,10 +100,14 @@ __device__ __forceinline__ void mulhilo32(uint32_t a, uint32_t b, uint32_t& hi, 
         : "=r"(hi), "=r"(lo) : "r"(a), "r"(b));
 }
 
+#ifndef HMC_PHILOX_ROUNDS
+#define HMC_PHILOX_ROUNDS 10  // experiments only; the production stream is Philox4x32-10
+#endif
+
 __device__ __forceinline__ uint4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2,
                                                uint32_t c3) {
 #pragma unroll
-    for (int i = 0; i < 10; ++i) {
+    for (int i = 0; i < HMC_PHILOX_ROUNDS; ++i) {
         const uint32_t k0 = kPhiloxK0 + (uint32_t)i * 0x9E3779B9u;
         const uint32_t k1 = kPhiloxK1 + (uint32_t)i * 0xBB67AE85u;
         uint32_t hi0, lo0, hi1, lo1;

@@ -37,6 +37,25 @@
 #ifndef HMC_SQRT_RSQ
 #define HMC_SQRT_RSQ 0
 #endif
+#ifndef HMC_PIPELINE_RNG
+#define HMC_PIPELINE_RNG 0   // generate step pair j+1's Philox block during pair j
+#endif
+#ifndef HMC_TRIPACK
+#define HMC_TRIPACK 1        // 3 steps per Philox block (23-bit radius, 19/18-bit angle)
+#endif
+#ifndef HMC_UNROLL_PAIRS
+#define HMC_UNROLL_PAIRS 1
+#endif
+#define HMC_PRAGMA_(x) _Pragma(#x)
+#define HMC_UNROLL_(n) HMC_PRAGMA_(unroll n)
+#define HMC_UNROLL(n) HMC_UNROLL_(n)
+#ifndef HMC_MIN_BLOCKS
+// 7 resident blocks (28 warps) per SM, up to 72 registers: fewer warps
+// contend less for the MIO/MUFU queue (tools/kernel_variants.py sweep:
+// 48 warps 11.1 ms, 28 warps 10.76 ms per 2^24 x 252 launch)
+#define HMC_MIN_BLOCKS 7
+#endif
+#define HMC_BOUNDS __launch_bounds__(kTile, HMC_MIN_BLOCKS)
 
 namespace hmc {
 
@@ -99,6 +118,58 @@ __device__ __forceinline__ float one_to_two(uint32_t x) {
 
 // Box-Muller on two Philox words; returns the step shocks
 //   z1l = sqrt(dt) z1 log2(e),   sz2 = sigma sqrt(dt) (rho z1 + sqrt(1-rho^2) zb)
+__device__ __forceinline__ void sincos_turns(float fa, uint32_t sgn, float& sn, float& cs) {
+#if HMC_SINCOS_POLY
+    // angle in [-pi/2, pi/2) from fa in [1, 2), sin/cos by Taylor polynomials
+    // (abs err 6e-8); a random sign bit (bit 31 of sgn) flips cos to cover
+    // the left half circle
+    const float r = fmaf(fa, 2.0f, -3.0f);                   // [-1, 1)
+    const float r2 = r * r;
+    float ps = -3.598843235212084e-06f;
+    ps = fmaf(ps, r2, 1.6044118478735975e-04f);
+    ps = fmaf(ps, r2, -4.681754135318687e-03f);
+    ps = fmaf(ps, r2, 7.969262624616703e-02f);
+    ps = fmaf(ps, r2, -6.459640975062462e-01f);
+    ps = fmaf(ps, r2, 1.5707963267948966f);
+    sn = ps * r;
+    float pc = 4.710874778818169e-07f;
+    pc = fmaf(pc, r2, -2.5202042373060596e-05f);
+    pc = fmaf(pc, r2, 9.192602748394263e-04f);
+    pc = fmaf(pc, r2, -2.0863480763352957e-02f);
+    pc = fmaf(pc, r2, 2.53669507901048e-01f);
+    pc = fmaf(pc, r2, -1.2337005501361697f);
+    pc = fmaf(pc, r2, 1.0f);
+    cs = __uint_as_float(__float_as_uint(pc) ^ (sgn & 0x80000000u));
+#else
+    const float th = fmaf(fa, 6.28318530717958647692f, -9.42477796076937971538f);
+    sn = __sinf(th);                                         // th in [-pi, pi)
+    cs = __cosf(th);
+    (void)sgn;
+#endif
+}
+
+__device__ __forceinline__ void box_muller_f(float fr, float fa, uint32_t sgn, const KernelArgs& a,
+                                             float& z1l, float& sz2) {
+    const float u1 = 2.0f - fr;                              // (0, 1]
+    const float R = sqrta(lg2a(u1) * a.f_bm2);               // sqrt(dt) sqrt(-2 ln u1) log2 e
+    float sn, cs;
+    sincos_turns(fa, sgn, sn, cs);
+    z1l = R * cs;
+    sz2 = R * fmaf(a.f_cA, cs, a.f_cB * sn);
+}
+
+// three Box-Muller steps from one 128-bit Philox block: radii from the top
+// 23 bits of w0, w1, w2; angles from w3[31:13], w3[12:0]|w0[8:3],
+// w1[8:0]|w2[8:0] (19, 19 and 18 bits); w0[2:0] left as spare sign bits
+__device__ __forceinline__ void tri_unpack(const uint4 w, float (&fr)[3], float (&fa)[3]) {
+    fr[0] = one_to_two(w.x);
+    fr[1] = one_to_two(w.y);
+    fr[2] = one_to_two(w.z);
+    fa[0] = __uint_as_float(((w.w >> 9) & 0x007FFFF0u) | 0x3f800000u);
+    fa[1] = __uint_as_float(((w.w << 10) & 0x007FFC00u) | ((w.x << 1) & 0x000003F0u) | 0x3f800000u);
+    fa[2] = __uint_as_float(((w.y << 14) & 0x007FC000u) | ((w.z << 5) & 0x00003FE0u) | 0x3f800000u);
+}
+
 __device__ __forceinline__ void box_muller(uint32_t xr, uint32_t xa, const KernelArgs& a,
                                            float& z1l, float& sz2) {
     const float u1 = 2.0f - one_to_two(xr);                  // (0, 1]
@@ -220,7 +291,7 @@ __device__ __forceinline__ void step(PathState32& st, int k, float z1l, float sz
 }
 
 template <int FIX, bool GREEKS, int SAMPLER>
-__global__ void __launch_bounds__(kTile) fast_greeks_kernel(const KernelArgs a,
+__global__ void HMC_BOUNDS fast_greeks_kernel(const KernelArgs a,
                                                             double* __restrict__ tiles,
                                                             long long n_tiles) {
     const int run = blockIdx.y;
@@ -228,6 +299,11 @@ __global__ void __launch_bounds__(kTile) fast_greeks_kernel(const KernelArgs a,
     const bool live = path < a.path_hi;
     const long long p = live ? path : a.path_lo;
 
+#ifdef HMC_SMEM_PAD
+    // experiments: cap resident blocks per SM through shared memory
+    __shared__ volatile char occupancy_pad[HMC_SMEM_PAD];
+    if (threadIdx.x == 0) occupancy_pad[0] = 0;
+#endif
     PathState32 st;
     st.v0 = a.f_v0;
     st.vu = a.f_vu;
@@ -241,11 +317,46 @@ __global__ void __launch_bounds__(kTile) fast_greeks_kernel(const KernelArgs a,
         const unsigned long long key_run = derive(a.root_key, (unsigned long long)run);
         const uint32_t c1 = (uint32_t)p;
         const uint32_t c2 = (uint32_t)key_run, c3 = (uint32_t)(key_run >> 32);
-        const int npairs = a.n_sim >> 1;
+#if HMC_TRIPACK
+        const int ntri = a.n_sim / 3;
         int k = 1;
 #pragma unroll 1
-        for (int j = 0; j < npairs; ++j) {
+        for (int j = 0; j < ntri; ++j) {
             const uint4 x = philox4x32_10((uint32_t)j, c1, c2, c3);
+            float fr[3], fa[3];
+            tri_unpack(x, fr, fa);
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                float z1l, sz2;
+                box_muller_f(fr[i], fa[i], x.x << (31 - i), a, z1l, sz2);
+                step<FIX, GREEKS>(st, k + i, z1l, sz2, a);
+            }
+            k += 3;
+        }
+        if (k <= a.n_sim) {
+            const uint4 x = philox4x32_10((uint32_t)ntri, c1, c2, c3);
+            float fr[3], fa[3];
+            tri_unpack(x, fr, fa);
+            for (int i = 0; k + i <= a.n_sim; ++i) {
+                float z1l, sz2;
+                box_muller_f(fr[i], fa[i], x.x << (31 - i), a, z1l, sz2);
+                step<FIX, GREEKS>(st, k + i, z1l, sz2, a);
+            }
+        }
+#else
+        const int npairs = a.n_sim >> 1;
+        int k = 1;
+#if HMC_PIPELINE_RNG
+        uint4 xn = philox4x32_10(0u, c1, c2, c3);
+#endif
+        HMC_UNROLL(HMC_UNROLL_PAIRS)
+        for (int j = 0; j < npairs; ++j) {
+#if HMC_PIPELINE_RNG
+            const uint4 x = xn;
+            xn = philox4x32_10((uint32_t)(j + 1), c1, c2, c3);
+#else
+            const uint4 x = philox4x32_10((uint32_t)j, c1, c2, c3);
+#endif
             float z1l, sz2;
             box_muller(x.x, x.y, a, z1l, sz2);
             step<FIX, GREEKS>(st, k, z1l, sz2, a);
@@ -259,6 +370,7 @@ __global__ void __launch_bounds__(kTile) fast_greeks_kernel(const KernelArgs a,
             box_muller(x.x, x.y, a, z1l, sz2);
             step<FIX, GREEKS>(st, k, z1l, sz2, a);
         }
+#endif
     } else {
         // engine.py:100: run r uses Sobol rows 1 + r*n_paths + path
         const uint32_t n = (uint32_t)(1 + (long long)run * a.n_paths + p);

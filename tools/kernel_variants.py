@@ -20,10 +20,12 @@ VDIR = os.path.join(ROOT, "paper_2309_10477_b200", "_variants")
 
 VARIANTS = {
     "base": {},
-    "rsq": {"HMC_SQRT_RSQ": 1},
     "sincos": {"HMC_SINCOS_POLY": 1},
     "ex2x1": {"HMC_EX2_POLY": 1},
-    "rsq_ex2x1": {"HMC_SQRT_RSQ": 1, "HMC_EX2_POLY": 1},
+    "ex2x2": {"HMC_EX2_POLY": 2},
+    "rsq": {"HMC_SQRT_RSQ": 1},
+    "lb8": {"HMC_MIN_BLOCKS": 8},
+    "ex2x1_lb8": {"HMC_EX2_POLY": 1, "HMC_MIN_BLOCKS": 8},
 }
 
 
