@@ -109,7 +109,8 @@ typedef struct hmc_sim {
                                 (hmc_sobol_init_directions layout)           */
     int32_t sobol_v_on_device; /* 1: sobol_v is a device pointer of the
                                   current device; 0: host pointer            */
-    int32_t reserved;
+    int32_t sobol_scramble;    /* sobol only: random digital shift per (run,
+                                  dimension) from the seed (randomised QMC)  */
 } hmc_sim;
 
 int hmc_abi_version(void);

@@ -63,7 +63,7 @@ class Sim(ctypes.Structure):
                 ("h_spot", ctypes.c_double), ("v0_up", ctypes.c_double),
                 ("v0_dn", ctypes.c_double), ("h_r", ctypes.c_double),
                 ("sobol_v", ctypes.POINTER(ctypes.c_uint32)),
-                ("sobol_v_on_device", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("sobol_v_on_device", ctypes.c_int32), ("sobol_scramble", ctypes.c_int32)]
 
 
 _lib = None

@@ -184,6 +184,7 @@ int prepare(const hmc_model* m, const hmc_product* pr, const hmc_sim* sim, Prepa
     a.path_hi = sim->path_hi;
     a.root_key = hmc_root_key(sim->seed);
     a.sobol_dim = 2 * sim->n_steps;
+    a.sobol_scramble = sim->sampler == HMC_SAMPLER_SOBOL && sim->sobol_scramble ? 1 : 0;
 
     fill_fp32_constants(a);
     std::vector<unsigned char> fix((size_t)sim->n_steps + 1, 0);

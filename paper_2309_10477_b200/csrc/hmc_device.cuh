@@ -56,6 +56,7 @@ struct KernelArgs {
     const float4* steps32;      // [n_steps + 1] fixing weights, see FixW
     const uint32_t* sobol_v;    // [30][sobol_dim]
     int sobol_dim;
+    int sobol_scramble;         // random digital shift per (run, dimension)
     // fp32 derived constants (host-computed in fp64, rounded once)
     float f_omkdt;   // 1 - kappa dt
     float f_ck0;     // kappa theta dt - milstein * sigma^2 dt / 4
@@ -137,6 +138,11 @@ __host__ __device__ __forceinline__ double uniform_at(unsigned long long key,
                                                       unsigned long long i) {
     return (double)(mix64(key + (i + 1) * 0x9E3779B97F4A7C15ULL) >> 11) *
            (1.0 / 9007199254740992.0);
+}
+
+// random digital shift (30 bits) of dimension d for the run with key key_run
+__host__ __device__ __forceinline__ uint32_t sobol_shift(unsigned long long key_run, int d) {
+    return (uint32_t)(mix64(key_run ^ ((unsigned long long)(d + 1) * 0x9E3779B97F4A7C15ULL)) >> 34);
 }
 
 // ---------------------------------------------------------------------------

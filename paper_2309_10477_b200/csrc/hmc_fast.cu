@@ -290,6 +290,86 @@ __device__ __forceinline__ void step(PathState32& st, int k, float z1l, float sz
     }
 }
 
+// ---------------------------------------------------------------------------
+// Sobol QMC driver (engine.py:97-101: run r uses points 1 + r*N + path).
+//
+// gray(n) = gray(n & ~31) ^ gray(n & 31) (no carries between the parts), so
+// the XOR of direction numbers splits into a warp-uniform high part U (the
+// warp's <= 2 aligned 32-point blocks) and a lane part T indexed by the
+// lane's 5-bit Gray code.  Both are rebuilt in shared memory for every
+// 64-step chunk of dimensions; the per-step cost is two LDS.64 + two XORs
+// instead of a 30-bit XOR per coordinate.  Optional random digital shift
+// (a.sobol_shift) per (run, dimension) for randomised QMC.
+// ---------------------------------------------------------------------------
+constexpr int kSobolSteps = 64;  // steps per table refill (128 dimensions)
+
+struct SobolTables {
+    uint2 T[kSobolSteps][32];          // lane parts, (dim 2q, dim 2q+1)
+    uint2 U[kWarps][2][kSobolSteps];   // per warp: blocks B1, B2
+};
+
+template <int FIX, bool GREEKS>
+__device__ __forceinline__ void sobol_paths(PathState32& st, int run, long long p, const KernelArgs& a) {
+    __shared__ SobolTables tab;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t n = (uint32_t)(1 + (long long)run * a.n_paths + p);
+    const uint32_t n0 = __shfl_sync(0xffffffffu, n, 0);
+    const uint32_t B1 = n0 & ~31u;
+    const uint32_t gB1 = B1 ^ (B1 >> 1), gB2 = (B1 + 32) ^ ((B1 + 32) >> 1);
+    const int which = ((n & ~31u) != B1) ? 1 : 0;
+    const uint32_t c = n & 31u, jl = c ^ (c >> 1);
+    const unsigned long long key_run = derive(a.root_key, (unsigned long long)run);
+    const uint32_t* __restrict__ V = a.sobol_v;
+    const int dim = a.sobol_dim;
+    const float c1 = a.f_sqdt * a.f_log2e;
+    const float cs = a.f_sigma * a.f_sqdt;
+
+#pragma unroll 1
+    for (int k0 = 1; k0 <= a.n_sim; k0 += kSobolSteps) {
+        const int m = min(kSobolSteps, a.n_sim - k0 + 1);
+        const int d0 = 2 * (k0 - 1);
+        __syncthreads();  // previous chunk fully consumed
+        // lane-part table: thread t owns dimension d0 + t, all 32 Gray codes
+        if (threadIdx.x < 2 * m) {
+            const int d = d0 + threadIdx.x;
+            uint32_t v[5];
+#pragma unroll
+            for (int b = 0; b < 5; ++b) v[b] = __ldg(V + b * dim + d);
+            uint32_t x[32];
+            x[0] = 0;
+#pragma unroll
+            for (int j = 1; j < 32; ++j) x[j] = x[j & (j - 1)] ^ v[__ffs(j) - 1];
+            uint32_t* col = reinterpret_cast<uint32_t*>(&tab.T[threadIdx.x >> 1][0]) + (threadIdx.x & 1);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) col[2 * j] = x[j];
+        }
+        // warp-uniform parts for this warp's two aligned blocks
+        for (int dd = lane; dd < 2 * m; dd += 32) {
+            const int d = d0 + dd;
+            uint32_t u1 = 0, u2d = 0;
+            for (int b = 4; b < kSobolBits; ++b) {
+                const uint32_t vb = ((gB1 | (gB1 ^ gB2)) >> b) & 1u ? __ldg(V + b * dim + d) : 0u;
+                if ((gB1 >> b) & 1u) u1 ^= vb;
+                if (((gB1 ^ gB2) >> b) & 1u) u2d ^= vb;
+            }
+            if (a.sobol_scramble) u1 ^= sobol_shift(key_run, d);
+            reinterpret_cast<uint32_t*>(&tab.U[warp][0][dd >> 1])[dd & 1] = u1;
+            reinterpret_cast<uint32_t*>(&tab.U[warp][1][dd >> 1])[dd & 1] = u1 ^ u2d;
+        }
+        __syncthreads();
+#pragma unroll 1
+        for (int q = 0; q < m; ++q) {
+            const uint2 t = tab.T[q][jl];
+            const uint2 u = tab.U[warp][which][q];
+            const float za = sobol_normal(t.x ^ u.x);
+            const float zb = sobol_normal(t.y ^ u.y);
+            const float z1l = c1 * za;
+            const float sz2 = cs * fmaf(a.f_rho, za, a.f_sq1mr2 * zb);
+            step<FIX, GREEKS>(st, k0 + q, z1l, sz2, a);
+        }
+    }
+}
+
 template <int FIX, bool GREEKS, int SAMPLER>
 __global__ void HMC_BOUNDS fast_greeks_kernel(const KernelArgs a,
                                                             double* __restrict__ tiles,
@@ -372,19 +452,7 @@ __global__ void HMC_BOUNDS fast_greeks_kernel(const KernelArgs a,
         }
 #endif
     } else {
-        // engine.py:100: run r uses Sobol rows 1 + r*n_paths + path
-        const uint32_t n = (uint32_t)(1 + (long long)run * a.n_paths + p);
-        const uint32_t gray = n ^ (n >> 1);
-        const float c1 = a.f_sqdt * a.f_log2e;
-        const float cs = a.f_sigma * a.f_sqdt;
-#pragma unroll 1
-        for (int k = 1; k <= a.n_sim; ++k) {
-            const float za = sobol_normal(sobol_coord(gray, a.sobol_v, a.sobol_dim, 2 * (k - 1)));
-            const float zb = sobol_normal(sobol_coord(gray, a.sobol_v, a.sobol_dim, 2 * k - 1));
-            const float z1l = c1 * za;
-            const float sz2 = cs * fmaf(a.f_rho, za, a.f_sq1mr2 * zb);
-            step<FIX, GREEKS>(st, k, z1l, sz2, a);
-        }
+        sobol_paths<FIX, GREEKS>(st, run, p, a);
     }
     if (FIX == kFixLast) fixing<GREEKS>(st, __ldg(a.steps32 + a.n_sim));
 

@@ -77,6 +77,8 @@ struct RefDraws {
     const uint32_t* v;
     int dim;
     const double* row;              // supplied uniforms (replay batch) or null
+    int scramble;                   // sobol: random digital shift (hmc_fast.cu sobol_shift)
+    unsigned long long key_run;
     __device__ __forceinline__ void get(int k, double& u1, double& u2) const {
         const int i = 2 * (k - 1);
         if (row) {
@@ -86,8 +88,13 @@ struct RefDraws {
             u1 = uniform_at(key, (unsigned long long)i);
             u2 = uniform_at(key, (unsigned long long)(i + 1));
         } else {
-            u1 = (double)sobol_coord(gray, v, dim, i) * (1.0 / 1073741824.0);
-            u2 = (double)sobol_coord(gray, v, dim, i + 1) * (1.0 / 1073741824.0);
+            uint32_t x1 = sobol_coord(gray, v, dim, i), x2 = sobol_coord(gray, v, dim, i + 1);
+            if (scramble) {
+                x1 ^= sobol_shift(key_run, i);
+                x2 ^= sobol_shift(key_run, i + 1);
+            }
+            u1 = (double)x1 * (1.0 / 1073741824.0);
+            u2 = (double)x2 * (1.0 / 1073741824.0);
         }
     }
 };
@@ -141,6 +148,8 @@ __global__ void __launch_bounds__(kTile) replay_greeks_kernel(const KernelArgs a
         dr.gray = n ^ (n >> 1);
         dr.v = a.sobol_v;
         dr.dim = a.sobol_dim;
+        dr.scramble = a.sobol_scramble;
+        dr.key_run = derive(a.root_key, (unsigned long long)run);
     }
     TrajD t0{a.s0, a.v0, 0.0, 0.0};
     TrajD tu{a.s0, a.v0_up, 0.0, 0.0};

@@ -85,7 +85,8 @@ class Job:
             precision=_lib.PRECISION[config.precision], want_greeks=int(want_greeks),
             n_steps=config.n_steps, n_runs=config.n_runs, n_paths=config.n_paths,
             path_lo=0, path_hi=config.n_paths, seed=config.seed & (2**64 - 1),
-            h_spot=h_spot, v0_up=v_up, v0_dn=v_dn, h_r=h_r)
+            h_spot=h_spot, v0_up=v_up, v0_dn=v_dn, h_r=h_r,
+            sobol_scramble=int(bool(config.sobol_scramble)))
         self.sobol_host = None
         if config.sampler == "sobol":
             if 1 + config.n_runs * config.n_paths > 2 ** sobol.BITS:

@@ -296,6 +296,38 @@ class TestSobol:
         # inverse normal and arithmetic precision differ
         np.testing.assert_allclose(g["price"].per_run_values, ref, rtol=2e-4)
 
+    @pytest.mark.parametrize("n_paths,n_steps,scramble", [(1000, 16, False), (70001, 130, False),
+                                                          (4096, 252, False), (3333, 65, True)])
+    def test_fp32_sobol_matches_fp64_sobol(self, bench_params, n_paths, n_steps, scramble):
+        """The shared-memory Gray-code generator of the fp32 kernel feeds the
+        same points (and digital shifts) as the fp64 per-coordinate path:
+        per-run Asian Greeks agree to fp32 accuracy (a wrong coordinate
+        would move them by O(SE) ~ 1e-3)."""
+        spec = OptionSpec("asian_arithmetic", "call", 100.0, 1.0, 100.0,
+                          averaging_times=daily_fixings(1.0, n_steps))
+        kw = dict(scheme="milstein", sampler="sobol", sobol_highdim_ack=True, n_paths=n_paths,
+                  n_steps=n_steps, n_runs=3, seed=17, sobol_scramble=scramble)
+        a = greeks(bench_params, spec, SimConfig(**kw))
+        b = greeks(bench_params, spec, SimConfig(precision="fp64", **kw))
+        for q in ("price", "delta", "rho"):
+            np.testing.assert_allclose(a[q].per_run_values, b[q].per_run_values, rtol=2e-4, atol=1e-5,
+                                       err_msg=q)
+
+    def test_scrambled_sobol_unbiased(self, bench_params):
+        spec = OptionSpec("european", "call", 100.0, 1.0, 100.0)
+        q = price(bench_params, spec, SimConfig(scheme="milstein", sampler="sobol", sobol_highdim_ack=True,
+                                                 sobol_scramble=True, n_paths=2**16, n_steps=64,
+                                                 n_runs=32, seed=5))
+        ps = price(bench_params, spec, SimConfig(scheme="milstein", n_paths=2**20, n_steps=64, n_runs=8,
+                                                 seed=5))
+        se_q = q.std_error / math.sqrt(q.n_runs)
+        se_p = ps.std_error / math.sqrt(ps.n_runs)
+        assert _close_se(q.estimate, se_q, ps.estimate, se_p, k=4.0)
+        # the randomised-QMC spread is below the plain-MC spread at equal paths
+        mc = price(bench_params, spec, SimConfig(scheme="milstein", n_paths=2**16, n_steps=64,
+                                                 n_runs=32, seed=6))
+        assert q.std_error < mc.std_error
+
     def test_sobol_index_range_limit(self, params, euro_call):
         cfg = SimConfig(scheme="milstein", sampler="sobol", sobol_highdim_ack=True, n_paths=2**29,
                         n_steps=4, n_runs=3)
