@@ -151,7 +151,8 @@ int prepare(const hmc_model* m, const hmc_product* pr, const hmc_sim* sim, Prepa
         return fail(HMC_E_INVALID, "the Philox counter addresses at most 2^32 paths per run");
     if (sim->sampler == HMC_SAMPLER_SOBOL) {
         if (!sim->sobol_v) return fail(HMC_E_INVALID, "sobol sampler needs direction numbers");
-        if (1.0 + (double)sim->n_runs * (double)sim->n_paths > 1073741824.0)
+        const double blocks = sim->sobol_scramble ? 1.0 : (double)sim->n_runs;
+        if (1.0 + blocks * (double)sim->n_paths > 1073741824.0)
             return fail(HMC_E_INVALID, "sobol index range exceeds 2^30 points");
     }
 

@@ -204,14 +204,16 @@ __device__ __forceinline__ void box_muller(uint32_t xr, uint32_t xa, const Kerne
     sz2 = R * fmaf(a.f_cA, cs, a.f_cB * sn);
 }
 
-// Standard-normal quantile of the Sobol coordinate x * 2^-30 (x in [1, 2^30)):
+// Standard-normal quantile of the Sobol coordinate u = (x + half) 2^-30:
 // Giles' single-precision erfinv, z = sqrt(2) erfinv(2u - 1), with 4u(1-u)
 // formed from the distance to the nearer end so the tails keep precision.
-__device__ __forceinline__ float sobol_normal(uint32_t x) {
-    const int m = (int)(2u * x) - (1 << 30);                // (2u - 1) 2^30
-    const uint32_t t = min(x, (1u << 30) - x);              // min(u, 1-u) 2^30
-    const float xs = (float)m * 9.31322574615478515625e-10f;
-    const float tf = (float)t * 9.31322574615478515625e-10f;
+// half = 0 for the reference's unscrambled points (x >= 1 always); half = 1/2
+// for digitally shifted points, where x = 0 can occur.
+__device__ __forceinline__ float sobol_normal(uint32_t x, float half) {
+    const int m = (int)(2u * x) - (1 << 30);                // (2u - 1) 2^30 - 2 half
+    const uint32_t t = min(x, (1u << 30) - x);              // min(u, 1-u) 2^30 (- half)
+    const float xs = fmaf((float)m, 9.31322574615478515625e-10f, half * 1.86264514923095703125e-09f);
+    const float tf = ((float)t + half) * 9.31322574615478515625e-10f;
     float w = -0.69314718055994530942f * lg2a(4.0f * tf * (1.0f - tf));
     float p;
     if (w < 5.0f) {
@@ -312,7 +314,8 @@ template <int FIX, bool GREEKS>
 __device__ __forceinline__ void sobol_paths(PathState32& st, int run, long long p, const KernelArgs& a) {
     __shared__ SobolTables tab;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t n = (uint32_t)(1 + (long long)run * a.n_paths + p);
+    // scrambled (randomised QMC): every run re-uses points 1..N under its own shifts
+        const uint32_t n = (uint32_t)(1 + (a.sobol_scramble ? 0LL : (long long)run * a.n_paths) + p);
     const uint32_t n0 = __shfl_sync(0xffffffffu, n, 0);
     const uint32_t B1 = n0 & ~31u;
     const uint32_t gB1 = B1 ^ (B1 >> 1), gB2 = (B1 + 32) ^ ((B1 + 32) >> 1);
@@ -323,6 +326,7 @@ __device__ __forceinline__ void sobol_paths(PathState32& st, int run, long long 
     const int dim = a.sobol_dim;
     const float c1 = a.f_sqdt * a.f_log2e;
     const float cs = a.f_sigma * a.f_sqdt;
+    const float half = a.sobol_scramble ? 0.5f : 0.0f;
 
 #pragma unroll 1
     for (int k0 = 1; k0 <= a.n_sim; k0 += kSobolSteps) {
@@ -361,8 +365,8 @@ __device__ __forceinline__ void sobol_paths(PathState32& st, int run, long long 
         for (int q = 0; q < m; ++q) {
             const uint2 t = tab.T[q][jl];
             const uint2 u = tab.U[warp][which][q];
-            const float za = sobol_normal(t.x ^ u.x);
-            const float zb = sobol_normal(t.y ^ u.y);
+            const float za = sobol_normal(t.x ^ u.x, half);
+            const float zb = sobol_normal(t.y ^ u.y, half);
             const float z1l = c1 * za;
             const float sz2 = cs * fmaf(a.f_rho, za, a.f_sq1mr2 * zb);
             step<FIX, GREEKS>(st, k0 + q, z1l, sz2, a);

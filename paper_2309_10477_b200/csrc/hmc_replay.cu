@@ -89,12 +89,14 @@ struct RefDraws {
             u2 = uniform_at(key, (unsigned long long)(i + 1));
         } else {
             uint32_t x1 = sobol_coord(gray, v, dim, i), x2 = sobol_coord(gray, v, dim, i + 1);
-            if (scramble) {
+            double half = 0.0;  // reference points: x * 2^-30 exactly (x >= 1)
+            if (scramble) {     // shifted points can hit x = 0: cell midpoints
                 x1 ^= sobol_shift(key_run, i);
                 x2 ^= sobol_shift(key_run, i + 1);
+                half = 0.5;
             }
-            u1 = (double)x1 * (1.0 / 1073741824.0);
-            u2 = (double)x2 * (1.0 / 1073741824.0);
+            u1 = ((double)x1 + half) * (1.0 / 1073741824.0);
+            u2 = ((double)x2 + half) * (1.0 / 1073741824.0);
         }
     }
 };
@@ -144,7 +146,8 @@ __global__ void __launch_bounds__(kTile) replay_greeks_kernel(const KernelArgs a
         dr.key = derive(derive(key_run, (unsigned long long)p), 0ULL);
     } else {
         // engine.py:100: run r uses Sobol rows 1 + r*n_paths + path
-        const uint32_t n = (uint32_t)(1 + (long long)run * a.n_paths + p);
+        // scrambled (randomised QMC): every run re-uses points 1..N under its own shifts
+        const uint32_t n = (uint32_t)(1 + (a.sobol_scramble ? 0LL : (long long)run * a.n_paths) + p);
         dr.gray = n ^ (n >> 1);
         dr.v = a.sobol_v;
         dr.dim = a.sobol_dim;

@@ -89,7 +89,8 @@ class Job:
             sobol_scramble=int(bool(config.sobol_scramble)))
         self.sobol_host = None
         if config.sampler == "sobol":
-            if 1 + config.n_runs * config.n_paths > 2 ** sobol.BITS:
+            blocks = 1 if config.sobol_scramble else config.n_runs
+            if 1 + blocks * config.n_paths > 2 ** sobol.BITS:
                 raise UnsupportedProduct("sobol index range exceeds the 2^30-point sequence")
             self.sobol_host = sobol.directions(sobol_dimension(spec, config))
         self.n_runs = config.n_runs

@@ -313,6 +313,19 @@ class TestSobol:
             np.testing.assert_allclose(a[q].per_run_values, b[q].per_run_values, rtol=2e-4, atol=1e-5,
                                        err_msg=q)
 
+    def test_scrambled_sobol_finite_at_scale(self, bench_params):
+        """Shifted coordinates can be exactly 0 (x == shift): the quantile
+        must stay finite (2^21 points x 504 dimensions hits such cells)."""
+        spec = OptionSpec("asian_arithmetic", "call", 100.0, 1.0, 100.0,
+                          averaging_times=daily_fixings(1.0, 252))
+        for prec in ("fp32", "fp64"):
+            g = greeks(bench_params, spec, SimConfig(
+                scheme="milstein", sampler="sobol", sobol_highdim_ack=True, sobol_scramble=True,
+                n_paths=2**21, n_steps=252, n_runs=2, seed=2024, precision=prec))
+            for q in QN:
+                assert all(np.isfinite(g[q].per_run_values)), (prec, q)
+            assert abs(g["price"].estimate - 5.238) < 0.02
+
     def test_scrambled_sobol_unbiased(self, bench_params):
         spec = OptionSpec("european", "call", 100.0, 1.0, 100.0)
         q = price(bench_params, spec, SimConfig(scheme="milstein", sampler="sobol", sobol_highdim_ack=True,
