@@ -155,6 +155,49 @@ int hmc_discretised_batch_f64(const hmc_model* model, double s0, double T,
                               const int64_t* avg_idx, int64_t n_avg,
                               double* out, int32_t device);
 
+/* ---- strike x maturity surfaces (BASELINE config 5) ---------------------
+ * European and daily-average Asian calls on a strike grid at several
+ * maturities of ONE time grid, full Greeks, all from the same paths.
+ * Maturity m is the grid date mat_idx[m] (t = mat_idx[m] * dt); the Asian
+ * average for maturity m runs over grid dates t_1..t_{mat_idx[m]}.
+ * Output layout (HMC_NW = {sum, sum of squares} x 7 quantities, the single-
+ * product order above): out[run][style: 0 european, 1 asian][mat][strike][HMC_NW]. */
+#define HMC_SURF_MAX_STRIKES 128
+#define HMC_SURF_MAX_MATS 32
+#define HMC_SURF_VALS 23  /* moment rows per (style, maturity) */
+
+typedef struct hmc_surface_spec {
+    double spot;
+    double dt;               /* grid step (year fraction)                      */
+    const double* strikes;   /* HOST, strictly increasing, > 0                 */
+    int32_t n_strikes;       /* 1 .. HMC_SURF_MAX_STRIKES                      */
+    int32_t n_mats;          /* 1 .. HMC_SURF_MAX_MATS                         */
+    const int64_t* mat_idx;  /* HOST, strictly increasing grid indices >= 1;
+                                sim->n_steps must equal mat_idx[n_mats - 1]    */
+} hmc_surface_spec;
+
+/* int64 words of the fixed-point histogram accumulator for n_runs runs:
+ * n_runs * 2 * n_mats * HMC_SURF_VALS * (n_strikes + 1). */
+int64_t hmc_surface_acc_words(const hmc_surface_spec* spec, int32_t n_runs);
+/* device workspace bytes of hmc_surface_partials */
+int64_t hmc_surface_workspace_bytes(const hmc_surface_spec* spec, const hmc_sim* sim);
+
+/* ADD this slice's paths [path_lo, path_hi) into d_acc (device int64, zero
+ * it first; hmc_surface_acc_words words).  Integer accumulation: slices may
+ * be summed in any order / all-reduced across GPUs with identical results.
+ * sim: scheme euler|milstein, sampler pseudo, precision fp32; bumps as for
+ * hmc_greeks.  Asynchronous on `stream`. */
+int hmc_surface_partials(const hmc_model* model, const hmc_surface_spec* spec,
+                         const hmc_sim* sim, int64_t* d_acc, void* d_work, void* stream);
+
+/* HOST: accumulated histograms -> out[run][2][n_mats][n_strikes][HMC_NW]. */
+int hmc_surface_finalize(const hmc_model* model, const hmc_surface_spec* spec,
+                         const hmc_sim* sim, const int64_t* h_acc, double* out);
+
+/* Convenience: whole job on one device, synchronous, HOST output. */
+int hmc_surface(const hmc_model* model, const hmc_surface_spec* spec, const hmc_sim* sim,
+                double* h_out, int32_t device);
+
 /* Joe-Kuo direction numbers as used by scipy.stats.qmc.Sobol(scramble=False)
  * (30 bits): poly[dim], vinit[dim][18] from scipy's
  * _sobol_direction_numbers.npz -> v_out[30][dim] (HOST).  Point n of the

@@ -27,6 +27,7 @@ UNITS = {
     "hmc_api.cu": [],
     "hmc_fast.cu": [],
     "hmc_replay.cu": ["-fmad=false"],
+    "hmc_surface.cu": [],
 }
 
 

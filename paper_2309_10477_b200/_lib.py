@@ -40,7 +40,12 @@ EXPORTS = (
     "hmc_chunks_in_slice", "hmc_workspace_bytes", "hmc_greeks_chunks",
     "hmc_reduce_chunks", "hmc_greeks", "hmc_discretised_batch_f64",
     "hmc_sobol_init_directions", "hmc_root_key", "hmc_derive_key", "hmc_philox_check",
+    "hmc_surface_acc_words", "hmc_surface_workspace_bytes", "hmc_surface_partials",
+    "hmc_surface_finalize", "hmc_surface",
 )
+HMC_SURF_MAX_STRIKES = 128
+HMC_SURF_MAX_MATS = 32
+HMC_SURF_VALS = 23
 
 
 class Model(ctypes.Structure):
@@ -64,6 +69,12 @@ class Sim(ctypes.Structure):
                 ("v0_dn", ctypes.c_double), ("h_r", ctypes.c_double),
                 ("sobol_v", ctypes.POINTER(ctypes.c_uint32)),
                 ("sobol_v_on_device", ctypes.c_int32), ("sobol_scramble", ctypes.c_int32)]
+
+
+class SurfaceSpec(ctypes.Structure):
+    _fields_ = [("spot", ctypes.c_double), ("dt", ctypes.c_double),
+                ("strikes", ctypes.POINTER(ctypes.c_double)), ("n_strikes", ctypes.c_int32),
+                ("n_mats", ctypes.c_int32), ("mat_idx", ctypes.POINTER(ctypes.c_int64))]
 
 
 _lib = None
@@ -90,6 +101,12 @@ def _declare(L: ctypes.CDLL) -> None:
                                                      i32, ctypes.POINTER(ctypes.c_uint32)]),
         "hmc_philox_check": (ctypes.c_int, [ctypes.POINTER(ctypes.c_uint32), i32,
                                              ctypes.POINTER(ctypes.c_uint32), i32]),
+        "hmc_surface_acc_words": (i64, [ctypes.POINTER(SurfaceSpec), i32]),
+        "hmc_surface_workspace_bytes": (i64, [ctypes.POINTER(SurfaceSpec), pS]),
+        "hmc_surface_partials": (ctypes.c_int, [pM, ctypes.POINTER(SurfaceSpec), pS, vp, vp, vp]),
+        "hmc_surface_finalize": (ctypes.c_int, [pM, ctypes.POINTER(SurfaceSpec), pS,
+                                                ctypes.POINTER(i64), pd]),
+        "hmc_surface": (ctypes.c_int, [pM, ctypes.POINTER(SurfaceSpec), pS, pd, i32]),
         "hmc_root_key": (u64, [u64]),
         "hmc_derive_key": (u64, [u64, u64]),
     }

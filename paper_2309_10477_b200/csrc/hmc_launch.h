@@ -7,6 +7,55 @@
 
 namespace hmc {
 
+// ---- strike x maturity surface (hmc_surface.cu) ---------------------------
+constexpr int kSurfThreads = 1024;      // paths per tile (one block)
+constexpr int kSurfMaxStrikes = HMC_SURF_MAX_STRIKES;
+constexpr int kSurfMaxMats = HMC_SURF_MAX_MATS;
+// Per (style, maturity): kSurfVals rows of nK + 1 columns.
+// Rows 0..14 are bucketed moments, column = strike bucket c(x) = #{K_j < x};
+// a strike's sum over {x > K_j} is the suffix sum over columns > j:
+//    0 sum A    (key A(1+e))   1 sum A^2   (key A(1+e))
+//    2 N        (key A)        3 sum A      4 sum A^2     5 sum w   6 sum w^2   (w = tw - T A)
+//    7 N        (key A(1-e))   8 sum A      9 sum A^2
+//   10 sum g    (key min(Au, Ad), g = d (Au - Ad)/dv)   11 sum g^2
+//   12 N        (key Rm)      13 sum a     14 sum a^2  (a = (d+ Rp - d- Rm)/2h_r)
+// Rows 15..22 are per-STRIKE band moments (column = strike j), added for
+// every strike a path's bumped pair straddles -- the only regions where a
+// finite difference is not a K-free or K-linear function of the path:
+//   15/16 sum x, x^2, x = A(1+e) - K_j,  A(1-e) <= K_j < A(1+e)   (FD delta)
+//   17/18 sum x, x^2, x = Au - K_j,      Ad <= K_j < Au           (vega)
+//   19/20 sum x, x^2, x = Ad - K_j,      Au <= K_j < Ad           (vega)
+//   21/22 sum x, x^2, x = Rp - K_j,      Rm <= K_j < Rp           (FD rho)
+constexpr int kSurfVals = 23;
+constexpr int kSurfBucketRows = 15;
+constexpr float kSurfLinScale = 1024.0f;      // 2^10 fixed point for linear moments
+constexpr float kSurfQuadScale = 0.25f;       // 2^-2 for quadratic moments
+constexpr float kSurfBandScale = 65536.0f;    // 2^16 for the (small) band moments
+
+struct SurfMat {
+    int step;      // grid index of the maturity
+    float inv_n;   // 1 / step (daily-average weight)
+    float T;       // t_step
+    float ehp, ehm;  // e^{+h_r T}, e^{-h_r T}
+    float d, dp, dm; // e^{-r T}, e^{-(r +- h_r) T}
+};
+
+struct SurfArgs {
+    const float* strikes;
+    int nK;
+    const SurfMat* mats;
+    int n_mats;
+    unsigned long long* acc;  // [run][2][n_mats][kSurfVals][nK + 1] int64 fixed point
+    float eps_up, eps_dn;     // 1 +- h_spot / S0
+    float inv_dv;             // 1 / (v0_up - v0_dn)
+    int uniform;              // strikes equally spaced: k0 + j / inv_dk
+    float k0, inv_dk;
+    float inv_2hr;            // 1 / (2 h_r)
+};
+
+cudaError_t launch_surface(const KernelArgs& a, const SurfArgs& s, long long n_tiles, int grid_x,
+                           cudaStream_t stream);
+
 // fp32 production kernel (hmc_fast.cu): tiles[run][tile][HMC_NW]
 cudaError_t launch_fast_greeks(const KernelArgs& a, double* d_tiles, long long n_tiles,
                                cudaStream_t s);

@@ -1,0 +1,270 @@
+// hmc_path32.cuh -- fp32 path building blocks shared by the production
+// kernels (hmc_fast.cu: single-product Greeks; hmc_surface.cu: strike x
+// maturity surfaces): MUFU wrappers, Philox -> Box-Muller step shocks, the
+// Giles quantile for Sobol coordinates, and the regrouped Milstein/Euler
+// trajectory update with fixing accumulation.  See hmc_fast.cu for the
+// algebra and DESIGN.md section 4 for the measurements behind each choice.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "hmc_device.cuh"
+
+#ifndef HMC_SINCOS_POLY
+#define HMC_SINCOS_POLY 0
+#endif
+#ifndef HMC_EX2_POLY
+#define HMC_EX2_POLY 0
+#endif
+#ifndef HMC_SQRT_RSQ
+#define HMC_SQRT_RSQ 0
+#endif
+#ifndef HMC_PIPELINE_RNG
+#define HMC_PIPELINE_RNG 0   // generate step pair j+1's Philox block during pair j
+#endif
+#ifndef HMC_TRIPACK
+#define HMC_TRIPACK 1        // 3 steps per Philox block (23-bit radius, 19/18-bit angle)
+#endif
+#ifndef HMC_UNROLL_PAIRS
+#define HMC_UNROLL_PAIRS 1
+#endif
+#define HMC_PRAGMA_(x) _Pragma(#x)
+#define HMC_UNROLL_(n) HMC_PRAGMA_(unroll n)
+#define HMC_UNROLL(n) HMC_UNROLL_(n)
+
+namespace hmc {
+
+__device__ __forceinline__ float ex2a(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float lg2a(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float sqrta(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rsqrta(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// sqrt(v) of a variance (v >= 0): MUFU.SQRT, or v * MUFU.RSQ(v) (exact 0 at v = 0)
+__device__ __forceinline__ float sqrt_var(float v) {
+#if HMC_SQRT_RSQ
+    return v * rsqrta(fmaxf(v, 1e-30f));
+#else
+    return sqrta(v);
+#endif
+}
+
+// 2^x on the FMA pipe: x = j + f, |f| <= 1/2, 2^f by a degree-6 Taylor
+// polynomial (rel. err 1.6e-7), exponent added with one LEA.
+__device__ __forceinline__ float ex2_poly(float x) {
+    const float magic = 12582912.0f;  // 1.5 * 2^23: rounds to integer
+    x = fmaxf(x, -125.0f);            // keep the exponent add in range
+    const float m = x + magic;
+    const float f = x - (m - magic);
+    float p = 1.5403530393381606e-4f;
+    p = fmaf(p, f, 1.3333558146428441e-3f);
+    p = fmaf(p, f, 9.6181291076284772e-3f);
+    p = fmaf(p, f, 5.5504108664821576e-2f);
+    p = fmaf(p, f, 2.4022650695910071e-1f);
+    p = fmaf(p, f, 6.9314718055994531e-1f);
+    p = fmaf(p, f, 1.0f);
+    return __uint_as_float(__float_as_uint(p) + (__float_as_uint(m) << 23));
+}
+
+template <int POLY>
+__device__ __forceinline__ float ex2_sel(float x) {
+    if (POLY) return ex2_poly(x);
+    return ex2a(x);
+}
+
+// uniform in [1, 2) from the top 23 bits of x: one LEA.HI
+__device__ __forceinline__ float one_to_two(uint32_t x) {
+    return __uint_as_float((x >> 9) + 0x3f800000u);
+}
+
+// Box-Muller on two Philox words; returns the step shocks
+//   z1l = sqrt(dt) z1 log2(e),   sz2 = sigma sqrt(dt) (rho z1 + sqrt(1-rho^2) zb)
+__device__ __forceinline__ void sincos_turns(float fa, uint32_t sgn, float& sn, float& cs) {
+#if HMC_SINCOS_POLY
+    // angle in [-pi/2, pi/2) from fa in [1, 2), sin/cos by Taylor polynomials
+    // (abs err 6e-8); a random sign bit (bit 31 of sgn) flips cos to cover
+    // the left half circle
+    const float r = fmaf(fa, 2.0f, -3.0f);                   // [-1, 1)
+    const float r2 = r * r;
+    float ps = -3.598843235212084e-06f;
+    ps = fmaf(ps, r2, 1.6044118478735975e-04f);
+    ps = fmaf(ps, r2, -4.681754135318687e-03f);
+    ps = fmaf(ps, r2, 7.969262624616703e-02f);
+    ps = fmaf(ps, r2, -6.459640975062462e-01f);
+    ps = fmaf(ps, r2, 1.5707963267948966f);
+    sn = ps * r;
+    float pc = 4.710874778818169e-07f;
+    pc = fmaf(pc, r2, -2.5202042373060596e-05f);
+    pc = fmaf(pc, r2, 9.192602748394263e-04f);
+    pc = fmaf(pc, r2, -2.0863480763352957e-02f);
+    pc = fmaf(pc, r2, 2.53669507901048e-01f);
+    pc = fmaf(pc, r2, -1.2337005501361697f);
+    pc = fmaf(pc, r2, 1.0f);
+    cs = __uint_as_float(__float_as_uint(pc) ^ (sgn & 0x80000000u));
+#else
+    const float th = fmaf(fa, 6.28318530717958647692f, -9.42477796076937971538f);
+    sn = __sinf(th);                                         // th in [-pi, pi)
+    cs = __cosf(th);
+    (void)sgn;
+#endif
+}
+
+__device__ __forceinline__ void box_muller_f(float fr, float fa, uint32_t sgn, const KernelArgs& a,
+                                             float& z1l, float& sz2) {
+    const float u1 = 2.0f - fr;                              // (0, 1]
+    const float R = sqrta(lg2a(u1) * a.f_bm2);               // sqrt(dt) sqrt(-2 ln u1) log2 e
+    float sn, cs;
+    sincos_turns(fa, sgn, sn, cs);
+    z1l = R * cs;
+    sz2 = R * fmaf(a.f_cA, cs, a.f_cB * sn);
+}
+
+// three Box-Muller steps from one 128-bit Philox block: radii from the top
+// 23 bits of w0, w1, w2; angles from w3[31:13], w3[12:0]|w0[8:3],
+// w1[8:0]|w2[8:0] (19, 19 and 18 bits); w0[2:0] left as spare sign bits
+__device__ __forceinline__ void tri_unpack(const uint4 w, float (&fr)[3], float (&fa)[3]) {
+    fr[0] = one_to_two(w.x);
+    fr[1] = one_to_two(w.y);
+    fr[2] = one_to_two(w.z);
+    fa[0] = __uint_as_float(((w.w >> 9) & 0x007FFFF0u) | 0x3f800000u);
+    fa[1] = __uint_as_float(((w.w << 10) & 0x007FFC00u) | ((w.x << 1) & 0x000003F0u) | 0x3f800000u);
+    fa[2] = __uint_as_float(((w.y << 14) & 0x007FC000u) | ((w.z << 5) & 0x00003FE0u) | 0x3f800000u);
+}
+
+__device__ __forceinline__ void box_muller(uint32_t xr, uint32_t xa, const KernelArgs& a,
+                                           float& z1l, float& sz2) {
+    const float u1 = 2.0f - one_to_two(xr);                  // (0, 1]
+    const float R = sqrta(lg2a(u1) * a.f_bm2);               // sqrt(dt) sqrt(-2 ln u1) log2 e
+    float sn, cs;
+#if HMC_SINCOS_POLY
+    // angle in [-pi/2, pi/2) from the top 23 bits, sin/cos by Taylor
+    // polynomials (abs err 6e-8), cos sign from a spare (low) bit of xr
+    const float r = fmaf(one_to_two(xa), 2.0f, -3.0f);       // [-1, 1)
+    const float r2 = r * r;
+    float ps = -3.598843235212084e-06f;
+    ps = fmaf(ps, r2, 1.6044118478735975e-04f);
+    ps = fmaf(ps, r2, -4.681754135318687e-03f);
+    ps = fmaf(ps, r2, 7.969262624616703e-02f);
+    ps = fmaf(ps, r2, -6.459640975062462e-01f);
+    ps = fmaf(ps, r2, 1.5707963267948966f);
+    sn = ps * r;
+    float pc = 4.710874778818169e-07f;
+    pc = fmaf(pc, r2, -2.5202042373060596e-05f);
+    pc = fmaf(pc, r2, 9.192602748394263e-04f);
+    pc = fmaf(pc, r2, -2.0863480763352957e-02f);
+    pc = fmaf(pc, r2, 2.53669507901048e-01f);
+    pc = fmaf(pc, r2, -1.2337005501361697f);
+    pc = fmaf(pc, r2, 1.0f);
+    cs = __uint_as_float(__float_as_uint(pc) ^ (xr << 31));
+#else
+    const float th = fmaf(one_to_two(xa), 6.28318530717958647692f, -9.42477796076937971538f);
+    sn = __sinf(th);                                         // th in [-pi, pi)
+    cs = __cosf(th);
+#endif
+    z1l = R * cs;
+    sz2 = R * fmaf(a.f_cA, cs, a.f_cB * sn);
+}
+
+// Standard-normal quantile of the Sobol coordinate u = (x + half) 2^-30:
+// Giles' single-precision erfinv, z = sqrt(2) erfinv(2u - 1), with 4u(1-u)
+// formed from the distance to the nearer end so the tails keep precision.
+// half = 0 for the reference's unscrambled points (x >= 1 always); half = 1/2
+// for digitally shifted points, where x = 0 can occur.
+__device__ __forceinline__ float sobol_normal(uint32_t x, float half) {
+    const int m = (int)(2u * x) - (1 << 30);                // (2u - 1) 2^30 - 2 half
+    const uint32_t t = min(x, (1u << 30) - x);              // min(u, 1-u) 2^30 (- half)
+    const float xs = fmaf((float)m, 9.31322574615478515625e-10f, half * 1.86264514923095703125e-09f);
+    const float tf = ((float)t + half) * 9.31322574615478515625e-10f;
+    float w = -0.69314718055994530942f * lg2a(4.0f * tf * (1.0f - tf));
+    float p;
+    if (w < 5.0f) {
+        w = w - 2.5f;
+        p = 2.81022636e-08f;
+        p = fmaf(p, w, 3.43273939e-07f);
+        p = fmaf(p, w, -3.5233877e-06f);
+        p = fmaf(p, w, -4.39150654e-06f);
+        p = fmaf(p, w, 0.00021858087f);
+        p = fmaf(p, w, -0.00125372503f);
+        p = fmaf(p, w, -0.00417768164f);
+        p = fmaf(p, w, 0.246640727f);
+        p = fmaf(p, w, 1.50140941f);
+    } else {
+        w = sqrta(w) - 3.0f;
+        p = -0.000200214257f;
+        p = fmaf(p, w, 0.000100950558f);
+        p = fmaf(p, w, 0.00134934322f);
+        p = fmaf(p, w, -0.00367342844f);
+        p = fmaf(p, w, 0.00573950773f);
+        p = fmaf(p, w, -0.0076224613f);
+        p = fmaf(p, w, 0.00943887047f);
+        p = fmaf(p, w, 1.00167406f);
+        p = fmaf(p, w, 2.83297682f);
+    }
+    return 1.41421356237309504880f * p * xs;
+}
+
+struct PathState32 {
+    float v0, L0, A0;  // base trajectory
+    float vu, Lu, Au;  // v0 + h
+    float vd, Ld, Ad;  // v0 - h (floored at 0)
+    float T1, Dp, Dm;  // base: sum S t, sum S expm1(h t), sum S expm1(-h t)
+};
+
+__device__ __forceinline__ void traj_step(float& v, float& L, float z1l, float sz2, float ck,
+                                          const KernelArgs& a) {
+    const float s = sqrt_var(v);
+    L = fmaf(s, z1l, L);
+    L = fmaf(v, a.f_nhdt2, L);
+    v = fmaxf(fmaf(s, sz2, fmaf(v, a.f_omkdt, ck)), 0.0f);
+}
+
+template <bool GREEKS>
+__device__ __forceinline__ void advance(PathState32& st, float z1l, float sz2, const KernelArgs& a) {
+    const float ck = fmaf(sz2 * sz2, a.f_cmil2, a.f_ck0);
+    traj_step(st.v0, st.L0, z1l, sz2, ck, a);
+    if (GREEKS) {
+        traj_step(st.vu, st.Lu, z1l, sz2, ck, a);
+        traj_step(st.vd, st.Ld, z1l, sz2, ck, a);
+    }
+}
+
+template <bool GREEKS>
+__device__ __forceinline__ void fixing(PathState32& st, const float4 w) {
+    const float P = ex2_sel<(HMC_EX2_POLY >= 3)>(st.L0);
+    st.A0 = fmaf(P, w.x, st.A0);
+    if (GREEKS) {
+        st.T1 = fmaf(P, w.y, st.T1);
+        st.Dp = fmaf(P, w.z, st.Dp);
+        st.Dm = fmaf(P, w.w, st.Dm);
+        st.Au = fmaf(ex2_sel<(HMC_EX2_POLY >= 1)>(st.Lu), w.x, st.Au);
+        st.Ad = fmaf(ex2_sel<(HMC_EX2_POLY >= 2)>(st.Ld), w.x, st.Ad);
+    }
+}
+
+template <int FIX, bool GREEKS>
+__device__ __forceinline__ void step(PathState32& st, int k, float z1l, float sz2,
+                                     const KernelArgs& a) {
+    advance<GREEKS>(st, z1l, sz2, a);
+    if (FIX == kFixEvery) {
+        fixing<GREEKS>(st, __ldg(a.steps32 + k));
+    } else if (FIX == kFixTable) {
+        const float4 w = __ldg(a.steps32 + k);
+        if (w.x != 0.0f) fixing<GREEKS>(st, w);
+    }
+}
+
+}  // namespace hmc

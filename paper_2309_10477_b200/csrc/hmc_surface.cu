@@ -1,0 +1,212 @@
+// hmc_surface.cu -- strike x maturity surfaces of European and daily-average
+// Asian calls with full Greeks from ONE set of simulated paths
+// (BASELINE config 5: 64 strikes x 8 maturities, both styles, 2^22 paths).
+//
+// Every (strike, maturity, style) shares the same paths (common random
+// numbers): the paths are simulated once to the last maturity with the
+// production step (hmc_path32.cuh); at each maturity checkpoint every path
+// drops its observables into per-maturity HISTOGRAMS keyed by the strike
+// bucket c(x) = #{j : K_j < x}.  Because a call payoff is linear in the
+// underlying above the strike,
+//     sum_paths (A - K_j)^+ = S1(A > K_j) - K_j N(A > K_j),
+// every per-strike sum and sum of squares of every estimator (price,
+// pathwise Delta/Rho, FD Gamma/Delta/Vega/Rho) follows from suffix sums of a
+// few bucketed moments (hmc_api.cu surface_finalize).  Cost per path and
+// maturity is O(log K) instead of O(K).
+//
+// Histograms are integer fixed point (linear moments 2^-10, quadratic 2^2,
+// counts exact; int32 per block, int64 per run): integer addition is
+// associative, so block order, grid size and GPU count cannot change a
+// single bit of the result -- multi-GPU runs all-reduce the integer
+// histograms.  Rounding to the grid is unbiased (round to nearest) and
+// ~1e-3 of a per-path value, far below the Monte Carlo noise.
+#include <cuda_runtime.h>
+
+#include "hmc_device.cuh"
+#include "hmc_launch.h"
+#include "hmc_path32.cuh"
+
+namespace hmc {
+
+// number of strikes strictly below x.  Uniform strike grids (the usual
+// surface) take an arithmetic guess and one exact correction step each way
+// against the stored strikes; otherwise an unrolled branch-free lower-bound
+// descent over <= 128 strikes.
+__device__ __forceinline__ int strike_bucket(const float* sK, int pow2, int nK, float x,
+                                             const SurfArgs& s) {
+    if (s.uniform) {
+        int c = (int)floorf((x - s.k0) * s.inv_dk) + 1;
+        c = min(max(c, 0), nK);
+        if (c > 0 && !(sK[c - 1] < x)) --c;
+        if (c < nK && sK[c] < x) ++c;
+        return c;
+    }
+    int pos = 0;
+#pragma unroll
+    for (int step = 128; step > 0; step >>= 1) {
+        const int cand = pos + step;
+        if (step <= pow2 && cand <= nK && sK[cand - 1] < x) pos = cand;
+    }
+    return pos;
+}
+
+// Block histograms are int32 fixed point updated with native shared-memory
+// atomics (64-bit shared atomics are CAS loops on sm_100).  A value whose
+// scaled magnitude reaches 2^20 bypasses the block histogram and goes
+// straight to the int64 run accumulator (native global RED), so 1024 paths
+// can never overflow an int32 bucket (1024 * 2^20 = 2^30).  The float ->
+// int conversion is the 1.5*2^23 magic add (FMA pipe, no XU conversion).
+__device__ __forceinline__ void hist_add(int* h, unsigned long long* gdirect, int nb, int v, int c,
+                                         float x, float scale) {
+    const float y = x * scale;
+    if (fabsf(y) < 1048576.0f) {
+        const int q = __float_as_int(y + 12582912.0f) - 0x4B400000;  // round to nearest
+        if (q) atomicAdd(h + v * nb + c, q);
+    } else {
+        atomicAdd(gdirect + v * nb + c, (unsigned long long)__float2ll_rn(y));
+    }
+}
+
+__device__ __forceinline__ void hist_count(int* h, int nb, int v, int c) {
+    atomicAdd(h + v * nb + c, 1);
+}
+
+// add moments of x - K_j for every strike j in [lo, hi) (a bumped pair
+// straddling those strikes; usually zero or one strike)
+__device__ __forceinline__ void band_add(int* h, unsigned long long* g64, int nb, const float* sK,
+                                         int row, int lo, int hi, float x) {
+    for (int j = lo; j < hi; ++j) {
+        const float e = x - sK[j];
+        hist_add(h, g64, nb, row, j, e, kSurfBandScale);
+        hist_add(h, g64, nb, row + 1, j, e * e, kSurfBandScale);
+    }
+}
+
+// one style at one maturity (row layout in hmc_launch.h)
+__device__ __forceinline__ void surface_update(int* h, unsigned long long* g64, int nb, const float* sK,
+                                               int pow2, int nK, const SurfArgs& s, float d, float A,
+                                               float Au, float Ad, float Rp, float Rm, float w,
+                                               float al) {
+    const float L = kSurfLinScale, Q = kSurfQuadScale;
+    const float Aup = A * s.eps_up, Adn = A * s.eps_dn;
+    const int cu = strike_bucket(sK, pow2, nK, Aup, s);
+    hist_add(h, g64, nb, 0, cu, A, L); hist_add(h, g64, nb, 1, cu, A * A, Q);
+    const int c1 = strike_bucket(sK, pow2, nK, A, s);
+    hist_count(h, nb, 2, c1); hist_add(h, g64, nb, 3, c1, A, L); hist_add(h, g64, nb, 4, c1, A * A, Q);
+    hist_add(h, g64, nb, 5, c1, w, L); hist_add(h, g64, nb, 6, c1, w * w, Q);
+    const int cd = strike_bucket(sK, pow2, nK, Adn, s);
+    hist_count(h, nb, 7, cd); hist_add(h, g64, nb, 8, cd, A, L); hist_add(h, g64, nb, 9, cd, A * A, Q);
+    band_add(h, g64, nb, sK, 15, cd, cu, Aup);
+    const int cvu = strike_bucket(sK, pow2, nK, Au, s), cvd = strike_bucket(sK, pow2, nK, Ad, s);
+    const float gv = d * (Au - Ad) * s.inv_dv;
+    const int cmin = min(cvu, cvd);
+    hist_add(h, g64, nb, 10, cmin, gv, L); hist_add(h, g64, nb, 11, cmin, gv * gv, Q);
+    band_add(h, g64, nb, sK, 17, cvd, cvu, Au);
+    band_add(h, g64, nb, sK, 19, cvu, cvd, Ad);
+    const int cp = strike_bucket(sK, pow2, nK, Rp, s), cm = strike_bucket(sK, pow2, nK, Rm, s);
+    hist_count(h, nb, 12, cm); hist_add(h, g64, nb, 13, cm, al, L); hist_add(h, g64, nb, 14, cm, al * al, Q);
+    band_add(h, g64, nb, sK, 21, cm, cp, Rp);
+}
+
+__device__ __forceinline__ void surface_checkpoint(const PathState32& st, const KernelArgs& a,
+                                                   const SurfArgs& s, int m, bool live, int* hist,
+                                                   const float* sK, int pow2,
+                                                   unsigned long long* gacc) {
+    const int nb = s.nK + 1;
+    const int per_style = kSurfVals * nb;
+    unsigned long long* g_euro = gacc + ((size_t)0 * s.n_mats + m) * per_style;
+    unsigned long long* g_asian = gacc + ((size_t)1 * s.n_mats + m) * per_style;
+    if (live) {
+        const SurfMat mc = s.mats[m];
+        const float E = __ldg(a.steps32 + mc.step).x;       // S0 e^{r T_m}
+        // European: S_T of each trajectory; r bumps by e^{+-h T}, for which
+        // d+ Rp - d- Rm = 0 exactly (the FD numerator is -K (d+ - d-))
+        const float Ae = E * ex2a(st.L0);
+        surface_update(hist, g_euro, nb, sK, pow2, s.nK, s, mc.d, Ae, E * ex2a(st.Lu), E * ex2a(st.Ld),
+                       Ae * mc.ehp, Ae * mc.ehm, 0.0f, 0.0f);
+        // Asian: average of S over grid dates t_1..t_m;
+        // a = [A (d+ - d-) + (d+ D+ - d- D-)/N] / 2h_r, both terms same sign
+        const float inv = mc.inv_n;
+        const float Aa = st.A0 * inv;
+        const float al = (Aa * (mc.dp - mc.dm) + (mc.dp * st.Dp - mc.dm * st.Dm) * inv) * s.inv_2hr;
+        surface_update(hist + per_style, g_asian, nb, sK, pow2, s.nK, s, mc.d, Aa, st.Au * inv, st.Ad * inv,
+                       fmaf(st.Dp, inv, Aa), fmaf(st.Dm, inv, Aa), fmaf(st.T1, inv, -mc.T * Aa), al);
+    }
+    __syncthreads();
+    // flush this maturity's block histograms into the run accumulators
+    for (int i = threadIdx.x; i < 2 * per_style; i += blockDim.x) {
+        const int v = hist[i];
+        if (v) {
+            const int style = i / per_style, rest = i - style * per_style;
+            atomicAdd(gacc + ((size_t)style * s.n_mats + m) * per_style + rest,
+                      (unsigned long long)(long long)v);
+            hist[i] = 0;
+        }
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kSurfThreads, 1) surface_kernel(const KernelArgs a, const SurfArgs s,
+                                                                  long long n_tiles) {
+    extern __shared__ int hist[];  // [2][kSurfVals][nK + 1] int32 fixed point
+    __shared__ float sK[kSurfMaxStrikes];
+    const int nb = s.nK + 1;
+    for (int i = threadIdx.x; i < s.nK; i += blockDim.x) sK[i] = s.strikes[i];
+    for (int i = threadIdx.x; i < 2 * kSurfVals * nb; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    int pow2 = 1;
+    while (pow2 * 2 <= s.nK) pow2 *= 2;
+
+    const int run = blockIdx.y;
+    unsigned long long* gacc = s.acc + (size_t)run * 2 * s.n_mats * kSurfVals * nb;
+    const unsigned long long key_run = derive(a.root_key, (unsigned long long)run);
+    const uint32_t c2 = (uint32_t)key_run, c3 = (uint32_t)(key_run >> 32);
+
+#pragma unroll 1
+    for (long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const long long path = a.path_lo + tile * kSurfThreads + threadIdx.x;
+        const bool live = path < a.path_hi;
+        const uint32_t c1 = (uint32_t)(live ? path : a.path_lo);
+        PathState32 st;
+        st.v0 = a.f_v0;
+        st.vu = a.f_vu;
+        st.vd = a.f_vd;
+        st.L0 = st.Lu = st.Ld = 0.0f;
+        st.A0 = st.Au = st.Ad = 0.0f;
+        st.T1 = st.Dp = st.Dm = 0.0f;
+        int m = 0, next = s.mats[0].step;
+#pragma unroll 1
+        for (int k0 = 1; k0 <= a.n_sim; k0 += 3) {
+            // same Philox counters as fast_greeks_kernel: (step triple, path, key_run)
+            const uint4 x = philox4x32_10((uint32_t)((k0 - 1) / 3), c1, c2, c3);
+            float fr[3], fa[3];
+            tri_unpack(x, fr, fa);
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                const int k = k0 + i;
+                if (k > a.n_sim) break;
+                float z1l, sz2;
+                box_muller_f(fr[i], fa[i], x.x << (31 - i), a, z1l, sz2);
+                step<kFixEvery, true>(st, k, z1l, sz2, a);
+                if (k == next) {
+                    surface_checkpoint(st, a, s, m, live, hist, sK, pow2, gacc);
+                    ++m;
+                    next = m < s.n_mats ? s.mats[m].step : 0x7fffffff;
+                }
+            }
+        }
+    }
+}
+
+cudaError_t launch_surface(const KernelArgs& a, const SurfArgs& s, long long n_tiles, int grid_x,
+                           cudaStream_t stream) {
+    const size_t smem = (size_t)2 * kSurfVals * (s.nK + 1) * sizeof(int);
+    cudaError_t e = cudaFuncSetAttribute(surface_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid((unsigned)grid_x, (unsigned)a.n_runs);
+    surface_kernel<<<grid, kSurfThreads, smem, stream>>>(a, s, n_tiles);
+    return cudaGetLastError();
+}
+
+}  // namespace hmc

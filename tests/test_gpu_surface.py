@@ -1,0 +1,96 @@
+"""Strike x maturity surfaces (BASELINE config 5): every surface point equals
+the single-product engine's estimate on the same paths; integer histograms
+make any split of the paths bit-identical."""
+
+import ctypes
+import math
+
+import numpy as np
+import pytest
+
+from oracle.semi_analytic import call_greeks
+from paper_2309_10477_b200 import (BENCH_PARAMS, HestonParams, OptionSpec, SimConfig, greeks,
+                                   surface, daily_fixings)
+from paper_2309_10477_b200 import _lib
+from paper_2309_10477_b200.surface import SurfaceJob
+
+pytestmark = pytest.mark.gpu
+
+STRIKES = [80.0, 92.5, 100.0, 104.0, 120.0]
+MATS = [0.25, 0.5, 1.0]
+QN = ("price", "delta", "rho", "gamma", "vega", "delta_fd", "rho_fd")
+
+
+def _cfg(n_steps, **kw):
+    base = dict(scheme="milstein", n_paths=40_000, n_steps=n_steps, n_runs=2, seed=31)
+    base.update(kw)
+    return SimConfig(**base)
+
+
+def test_surface_points_equal_single_product_engine():
+    p = HestonParams(**BENCH_PARAMS)
+    res = surface(p, STRIKES, MATS, _cfg(64))
+    for mi, T in enumerate(MATS):
+        n = int(round(T * 64))
+        for j, K in enumerate(STRIKES):
+            for style in ("european", "asian_arithmetic"):
+                dates = daily_fixings(T, n) if style != "european" else ()
+                g = greeks(p, OptionSpec(style, "call", K, T, 100.0, averaging_times=dates), _cfg(n))
+                for q in QN:
+                    est = res.estimate[style][q][mi, j]
+                    tol = 2e-5 if q in ("price", "delta", "rho") else 2e-3
+                    scale = max(abs(g[q].estimate), 1e-3)
+                    assert abs(est - g[q].estimate) <= tol * scale + 1e-6, (style, T, K, q, est,
+                                                                           g[q].estimate)
+                    se, se_ref = res.path_std_error[style][q][mi, j], g[q].path_std_error
+                    assert abs(se - se_ref) <= 2e-2 * se_ref + 1e-7, (style, T, K, q, se, se_ref)
+
+
+def test_split_paths_bit_identical():
+    p = HestonParams(**BENCH_PARAMS)
+    cfg = _cfg(64, n_paths=3 * 16384 + 77, n_runs=1)
+    job = SurfaceJob(p, STRIKES, MATS, cfg)
+    whole = job.run_device()
+    import torch
+    L = _lib.lib()
+    words = L.hmc_surface_acc_words(ctypes.byref(job.spec), 1)
+    acc = torch.zeros(words, dtype=torch.int64, device="cuda")
+    for lo, hi in ((16384, 3 * 16384 + 77), (0, 16384)):      # any order, any split
+        job.sim.path_lo, job.sim.path_hi = lo, hi
+        work = torch.empty(L.hmc_surface_workspace_bytes(ctypes.byref(job.spec), ctypes.byref(job.sim)),
+                           dtype=torch.uint8, device="cuda")
+        _lib.check(L.hmc_surface_partials(ctypes.byref(job.model), ctypes.byref(job.spec),
+                                          ctypes.byref(job.sim), ctypes.c_void_p(acc.data_ptr()),
+                                          ctypes.c_void_p(work.data_ptr()), None))
+        torch.cuda.synchronize()
+    out = np.zeros_like(whole)
+    h = acc.cpu().numpy()
+    _lib.check(L.hmc_surface_finalize(ctypes.byref(job.model), ctypes.byref(job.spec),
+                                      ctypes.byref(job.sim), h.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                      out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+    np.testing.assert_array_equal(out, whole)
+
+
+def test_european_surface_vs_semi_analytic():
+    p = HestonParams(**BENCH_PARAMS)
+    strikes = [90.0, 100.0, 110.0]
+    res = surface(p, strikes, [0.5, 1.0], SimConfig(scheme="milstein", n_paths=2**22, n_steps=252,
+                                                     n_runs=1, seed=8))
+    for mi, T in enumerate([0.5, 1.0]):
+        for j, K in enumerate(strikes):
+            sa = call_greeks(100.0, K, T, p.r, p.kappa, p.theta, p.sigma, p.rho, p.v0)
+            for q in ("price", "delta", "rho"):
+                est = res.estimate["european"][q][mi, j]
+                se = res.path_std_error["european"][q][mi, j]
+                assert abs(est - sa[q]) <= 4 * se, (T, K, q, est, sa[q], se)
+
+
+def test_validation():
+    p = HestonParams(**BENCH_PARAMS)
+    from paper_2309_10477_b200 import ValidationError, UnsupportedProduct
+    with pytest.raises(ValidationError):
+        surface(p, [100.0, 90.0], MATS, _cfg(64))
+    with pytest.raises(ValidationError):
+        surface(p, STRIKES, [0.3, 1.0], _cfg(64))
+    with pytest.raises(UnsupportedProduct):
+        surface(p, STRIKES, MATS, _cfg(64, precision="fp64"))
