@@ -64,6 +64,8 @@ class SurfaceJob:
         self.strikes = np.ascontiguousarray(strikes, dtype=np.float64)
         if not (1 <= self.strikes.size <= _lib.HMC_SURF_MAX_STRIKES):
             raise ValidationError(f"need 1..{_lib.HMC_SURF_MAX_STRIKES} strikes")
+        if not (np.all(self.strikes > 0) and np.all(np.diff(self.strikes) > 0)):
+            raise ValidationError("strikes must be positive and strictly increasing")
         if len(maturities) > _lib.HMC_SURF_MAX_MATS:
             raise ValidationError(f"need at most {_lib.HMC_SURF_MAX_MATS} maturities")
         dt, idx = _grid(maturities, config)

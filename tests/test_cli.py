@@ -51,6 +51,12 @@ class TestParsing:
         assert flat["bump_v0"] == 0.02 and flat["kappa"] == 6.21 and flat["format"] == "table"
         json.dumps(flat)
 
+    def test_surface_grids(self):
+        assert cli.parse_grid("80:121:5") == [80.0, 85.0, 90.0, 95.0, 100.0, 105.0, 110.0, 115.0, 120.0]
+        assert cli.parse_grid("0.25,0.5") == [0.25, 0.5]
+        _, _, merged = parse_config(["surface", "--strikes", "90,100", "--maturities", "0.5,1"])
+        assert merged["_strikes"] == [90.0, 100.0] and merged["_maturities"] == [0.5, 1.0]
+
     def test_reference_stream_points(self):
         import oracle
         u = cli._reference_uniforms(7, 16)
@@ -105,6 +111,13 @@ class TestOutputs:
         row = json.loads(out.strip().splitlines()[0])
         assert code == 0 and row["quantity"] == "price" and row["precision"] == "fp64"
         assert row["mean"] > 0
+
+    def test_surface_csv(self, capsys):
+        code, out, _ = run(capsys, ["surface", "--strikes", "90:111:10", "--maturities", "0.5,1",
+                                    "--steps", "32", "--paths", "8192", "--runs", "2", "--s0", "100"])
+        lines = out.strip().splitlines()
+        assert code == 0 and lines[0].startswith("style,maturity,strike,quantity")
+        assert len(lines) == 1 + 2 * 7 * 2 * 3
 
     def test_bench_sweep_and_points(self, capsys, tmp_path):
         pts = tmp_path / "pts.csv"

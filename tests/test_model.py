@@ -116,3 +116,21 @@ class TestEngineValidation:
         p0 = HestonParams(params.kappa, params.theta, params.sigma, params.rho, params.r, 0.0)
         _, up, dn, _ = engine.bump_sizes(p0, euro_call, SimConfig())
         assert dn == 0.0 and up > 0.0
+
+
+class TestSurfaceValidation:
+    """Rejected on the host before any device work."""
+
+    def test_bad_grids(self, params):
+        from paper_2309_10477_b200 import surface
+        cfg = SimConfig(scheme="milstein", n_steps=64, n_paths=1024, n_runs=1)
+        with pytest.raises(ValidationError):
+            surface(params, [100.0, 90.0], [0.5, 1.0], cfg)
+        with pytest.raises(ValidationError):
+            surface(params, [90.0, 100.0], [0.3, 1.0], cfg)      # off the dt = 1/64 grid
+        with pytest.raises(ValidationError):
+            surface(params, list(range(1, 200)), [1.0], cfg)     # > 128 strikes
+        with pytest.raises(UnsupportedProduct):
+            surface(params, [100.0], [1.0], SimConfig(scheme="exact"))
+        with pytest.raises(UnsupportedProduct):
+            surface(params, [100.0], [1.0], SimConfig(scheme="milstein", precision="fp64"))
