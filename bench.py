@@ -196,7 +196,8 @@ def run_b200(args) -> None:
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    distributed = "LOCAL_RANK" in os.environ  # launched by torch.distributed.run
+    if distributed:
         dist.init_process_group("nccl", device_id=dev)
     p, spec, cfg = workload()
     L = _lib.lib()
@@ -231,7 +232,7 @@ def run_b200(args) -> None:
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    if world > 1:
+    if distributed:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
@@ -240,12 +241,12 @@ def run_b200(args) -> None:
             step(e0, e1)
             e2.record(stream)
         torch.cuda.synchronize()
-    if world > 1:
+    if distributed:
         dist.barrier()
     step_ms = [e0.elapsed_time(e2) for e0, _, e2 in ev]
     kern_ms = [e0.elapsed_time(e1) for e0, e1, _ in ev]
     t = torch.tensor([sum(step_ms), sum(kern_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
+    if distributed:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_per_step = float(t[0]) / args.steps
     kernel_ms = float(t[1]) / args.steps
@@ -258,7 +259,7 @@ def run_b200(args) -> None:
     e2e_times = []
     g = None
     for i in range(0 if args.no_e2e else max(2, args.steps // 2) + 1):
-        if world > 1:
+        if distributed:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -266,7 +267,7 @@ def run_b200(args) -> None:
         e2e_times.append(time.perf_counter() - t0)
     e2e_s = sorted(e2e_times[1:])[len(e2e_times[1:]) // 2] if e2e_times else float("nan")
     te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if world > 1:
+    if distributed:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_s = float(te[0])
     h2d = (N_STEPS + 1) * (32 + 16) + job.avg_idx.nbytes
@@ -304,7 +305,7 @@ def run_b200(args) -> None:
         if world == 1 and not args.no_cpu:
             line["cpu_baseline"] = cpu_baseline_block()
         print(json.dumps(line))
-    if world > 1:
+    if distributed:
         dist.destroy_process_group()
 
 
