@@ -620,7 +620,6 @@ int hmc_surface_finalize(const hmc_model* model, const hmc_surface_spec* spec, c
     if (!h_acc || !out) return fail(HMC_E_INVALID, "h_acc / out is NULL");
     const KernelArgs& a = S.P.a;
     const int nK = spec->n_strikes, nb = nK + 1, V = HMC_SURF_VALS;
-    const double L = 1.0 / hmc::kSurfLinScale, Q = 1.0 / hmc::kSurfQuadScale;
     // row kind: 0 count, 1 linear, 2 quadratic, 3 band (layout: hmc_launch.h)
     static const int kind[HMC_SURF_VALS] = {1, 2, 0, 1, 2, 1, 2, 0, 1, 2, 1, 2, 0, 1, 2,
                                             3, 3, 3, 3, 3, 3, 3, 3};

@@ -22,6 +22,9 @@
 #ifndef HMC_PIPELINE_RNG
 #define HMC_PIPELINE_RNG 0   // generate step pair j+1's Philox block during pair j
 #endif
+#ifndef HMC_EX2_DELTA
+#define HMC_EX2_DELTA 0      // bumped trajectories' 2^L from the base one (guarded)
+#endif
 #ifndef HMC_TRIPACK
 #define HMC_TRIPACK 1        // 3 steps per Philox block (23-bit radius, 19/18-bit angle)
 #endif
@@ -250,8 +253,29 @@ __device__ __forceinline__ void fixing(PathState32& st, const float4 w) {
         st.T1 = fmaf(P, w.y, st.T1);
         st.Dp = fmaf(P, w.z, st.Dp);
         st.Dm = fmaf(P, w.w, st.Dm);
+#if HMC_EX2_DELTA
+        // the v0-bumped log-prices stay within |d| << 1 of the base one, so
+        // 2^{L+d} = 2^L (1 + d ln2 + (d ln2)^2/2 + (d ln2)^3/6) (rel. err
+        // < 6e-8 for |d| <= 0.05); a warp with any larger d uses MUFU.EX2
+        const float du = st.Lu - st.L0, dd = st.Ld - st.L0;
+        float Pu, Pd;
+        if (__all_sync(0xffffffffu, fmaxf(fabsf(du), fabsf(dd)) <= 0.05f)) {
+            auto e2 = [](float d) {
+                return fmaf(fmaf(fmaf(0.0555041086648216f, d, 0.2402265069591007f), d,
+                                 0.6931471805599453f), d, 1.0f);
+            };
+            Pu = P * e2(du);
+            Pd = P * e2(dd);
+        } else {
+            Pu = ex2a(st.Lu);
+            Pd = ex2a(st.Ld);
+        }
+        st.Au = fmaf(Pu, w.x, st.Au);
+        st.Ad = fmaf(Pd, w.x, st.Ad);
+#else
         st.Au = fmaf(ex2_sel<(HMC_EX2_POLY >= 1)>(st.Lu), w.x, st.Au);
         st.Ad = fmaf(ex2_sel<(HMC_EX2_POLY >= 2)>(st.Ld), w.x, st.Ad);
+#endif
     }
 }
 

@@ -181,6 +181,16 @@ __global__ void __launch_bounds__(kSurfThreads, 1) surface_kernel(const KernelAr
             const uint4 x = philox4x32_10((uint32_t)((k0 - 1) / 3), c1, c2, c3);
             float fr[3], fa[3];
             tri_unpack(x, fr, fa);
+            if (k0 + 2 < next) {
+                // no maturity inside this triple (next <= n_sim always): plain steps
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    float z1l, sz2;
+                    box_muller_f(fr[i], fa[i], x.x << (31 - i), a, z1l, sz2);
+                    step<kFixEvery, true>(st, k0 + i, z1l, sz2, a);
+                }
+                continue;
+            }
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
                 const int k = k0 + i;

@@ -20,12 +20,8 @@ VDIR = os.path.join(ROOT, "paper_2309_10477_b200", "_variants")
 
 VARIANTS = {
     "base": {},
-    "sincos": {"HMC_SINCOS_POLY": 1},
-    "ex2x1": {"HMC_EX2_POLY": 1},
-    "ex2x2": {"HMC_EX2_POLY": 2},
-    "rsq": {"HMC_SQRT_RSQ": 1},
-    "lb8": {"HMC_MIN_BLOCKS": 8},
-    "ex2x1_lb8": {"HMC_EX2_POLY": 1, "HMC_MIN_BLOCKS": 8},
+    "ex2delta": {"HMC_EX2_DELTA": 1},
+    "ex2delta_lb8": {"HMC_EX2_DELTA": 1, "HMC_MIN_BLOCKS": 8},
 }
 
 
