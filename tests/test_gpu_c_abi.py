@@ -1,0 +1,35 @@
+"""The C ABI from a plain C host: compile
+tests/c_abi/greeks_example.c against include/hmc.h, link libhmc.so, run it,
+and compare with the Python engine on the same job (same Philox stream)."""
+
+import os
+import shutil
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+from paper_2309_10477_b200 import BENCH_PARAMS, HestonParams, OptionSpec, SimConfig, daily_fixings, greeks
+
+pytestmark = pytest.mark.gpu
+
+
+def test_plain_c_host(tmp_path):
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    lib_dir = os.path.join(ROOT, "paper_2309_10477_b200")
+    exe = tmp_path / "greeks_example"
+    # libhmc.so has no SONAME prefix 'lib' issue: link by full path
+    subprocess.run([cc, "-O2", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "c_abi", "greeks_example.c"),
+                    os.path.join(lib_dir, "libhmc.so"), f"-Wl,-rpath,{lib_dir}", "-lm",
+                    "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe), str(2**20)], check=True, capture_output=True, text=True).stdout
+    rows = {ln.split()[0]: ln.split()[1:] for ln in out.strip().splitlines()}
+    p = HestonParams(**BENCH_PARAMS)
+    spec = OptionSpec("asian_arithmetic", "call", 100.0, 1.0, 100.0, averaging_times=daily_fixings(1.0, 252))
+    g = greeks(p, spec, SimConfig(scheme="milstein", n_paths=2**20, n_steps=252, n_runs=1, seed=42))
+    for q in ("price", "delta", "rho", "gamma", "vega", "delta_fd", "rho_fd"):
+        assert float(rows[q][0]) == pytest.approx(g[q].estimate, rel=1e-12, abs=1e-14), q
+    assert rows["put_greeks_rc"][0] == "-4"

@@ -20,8 +20,7 @@ VDIR = os.path.join(ROOT, "paper_2309_10477_b200", "_variants")
 
 VARIANTS = {
     "base": {},
-    "ex2delta": {"HMC_EX2_DELTA": 1},
-    "ex2delta_lb8": {"HMC_EX2_DELTA": 1, "HMC_MIN_BLOCKS": 8},
+    "noi2f": {"HMC_SOBOL_NOI2F": 1},
 }
 
 
@@ -42,7 +41,15 @@ sys.path.insert(0, %(root)r)
 from paper_2309_10477_b200 import _lib, engine, greeks
 import bench
 p, spec, cfg = bench.workload()
+import os as _os, dataclasses as _dc
+if _os.environ.get("HMC_VARIANT_SOBOL"):
+    cfg = _dc.replace(cfg, sampler="sobol", sobol_highdim_ack=True, sobol_scramble=True, n_paths=2**22)
 job = engine.Job(p, spec, cfg, True)
+if job.sobol_host is not None:
+    import numpy as _np
+    _v = _np.ascontiguousarray(job.sobol_host)
+    job.sim.sobol_v = _v.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))
+    job.sim.sobol_v_on_device = 0
 L = _lib.lib()
 work = torch.empty(L.hmc_workspace_bytes(ctypes.byref(job.sim)), dtype=torch.uint8, device="cuda")
 loc = torch.zeros((1, -(-cfg.n_paths // 16384), 14), dtype=torch.float64, device="cuda")
