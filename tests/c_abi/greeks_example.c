@@ -35,7 +35,7 @@ int main(int argc, char** argv) {
     for (int q = 0; q < HMC_NQ; ++q) {
         const double mean = out[2 * q] / n_paths;
         const double var = (out[2 * q + 1] - out[2 * q] * mean) / (n_paths - 1);
-        printf("%s %.12g %.6g\n", names[q], mean, sqrt(var > 0 ? var / n_paths : 0));
+        printf("%s %.17g %.6g\n", names[q], mean, sqrt(var > 0 ? var / n_paths : 0));
     }
     /* a usage error never touches the device */
     p.right = HMC_PUT;

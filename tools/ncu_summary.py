@@ -29,5 +29,9 @@ def summary(path):
 
 
 if __name__ == "__main__":
-    for p in sys.argv[1:]:
-        print(p, json.dumps(summary(p), indent=1))
+    args = [a for a in sys.argv[1:] if a != "--json"]
+    for p in args:
+        if "--json" in sys.argv:
+            print(json.dumps({"report": p.split("/")[-1], **summary(p)}, indent=1))
+        else:
+            print(p, json.dumps(summary(p), indent=1))
