@@ -52,6 +52,47 @@ def workload():
     return p, spec, cfg
 
 
+def secondary_workloads(reps: int = 3) -> dict:
+    """The other BASELINE configs on one GPU through the public API (CUDA
+    events around each call; host overhead included)."""
+    import numpy as np
+    import torch
+    from paper_2309_10477_b200 import (BENCH_PARAMS, HestonParams, OptionSpec, SimConfig, greeks,
+                                       surface, daily_fixings)
+    p = HestonParams(**BENCH_PARAMS)
+    euro = OptionSpec("european", "call", 100.0, 1.0, 100.0)
+    asian = OptionSpec("asian_arithmetic", "call", 100.0, 1.0, 100.0,
+                       averaging_times=daily_fixings(1.0, N_STEPS))
+    jobs = {
+        "c2_european_full_greeks_2^22x252": (
+            lambda: greeks(p, euro, SimConfig(scheme="milstein", n_paths=2**22, n_steps=252,
+                                              n_runs=1, seed=7)), 2**22 * 252),
+        "c4_sobol_rqmc_asian_full_greeks_2^22x252": (
+            lambda: greeks(p, asian, SimConfig(scheme="milstein", sampler="sobol",
+                                               sobol_highdim_ack=True, sobol_scramble=True,
+                                               n_paths=2**22, n_steps=252, n_runs=1, seed=7)),
+            2**22 * 252),
+        "c5_surface_64Kx8T_euro+asian_full_greeks_2^22x504": (
+            lambda: surface(p, np.arange(70.0, 134.0, 1.0), [0.25 * i for i in range(1, 9)],
+                            SimConfig(scheme="milstein", n_paths=2**22, n_steps=504, n_runs=1,
+                                      seed=7)), 2**22 * 504),
+    }
+    out = {}
+    for name, (fn, path_steps) in jobs.items():
+        fn()
+        ts = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms = sorted(ts)[len(ts) // 2]
+        out[name] = {"ms": ms, "path_steps_per_s": path_steps / (ms / 1e3)}
+    return out
+
+
 def config_block(n_gpus: int) -> dict:
     return {"workload": "asian_arith_call_daily_fixings_full_greeks",
             "paths": N_PATHS, "time_steps": N_STEPS, "fixings": N_STEPS, "scheme": "milstein",
@@ -304,6 +345,8 @@ def run_b200(args) -> None:
         }
         if world == 1 and not args.no_cpu:
             line["cpu_baseline"] = cpu_baseline_block()
+        if world == 1 and not args.no_e2e:
+            line["secondary"] = secondary_workloads()
         print(json.dumps(line))
     if distributed:
         dist.destroy_process_group()

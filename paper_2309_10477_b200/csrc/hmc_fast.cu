@@ -30,13 +30,16 @@
 
 #include "hmc_path32.cuh"
 
-#ifndef HMC_MIN_BLOCKS
-// 7 resident blocks (28 warps) per SM, up to 72 registers: fewer warps
-// contend less for the MIO/MUFU queue (tools/kernel_variants.py sweep:
-// 48 warps 11.1 ms, 28 warps 10.76 ms per 2^24 x 252 launch)
-#define HMC_MIN_BLOCKS 7
-#endif
+// Resident blocks per SM (register budget) by fixing mode, from
+// tools/kernel_variants.py sweeps on 2^24 x 252 full-Greeks launches:
+// daily-fixing Asian is MUFU-queue bound and prefers 7 blocks (28 warps,
+// 72 regs: 48 warps 11.1 ms -> 28 warps 10.7 ms); the European (one ex2 at
+// the end) prefers 10 blocks (8.55 -> 8.40 ms).
+#ifdef HMC_MIN_BLOCKS
 #define HMC_BOUNDS __launch_bounds__(kTile, HMC_MIN_BLOCKS)
+#else
+#define HMC_BOUNDS __launch_bounds__(kTile, (FIX == kFixLast ? 10 : 7))
+#endif
 
 namespace hmc {
 

@@ -20,7 +20,10 @@ VDIR = os.path.join(ROOT, "paper_2309_10477_b200", "_variants")
 
 VARIANTS = {
     "base": {},
-    "noi2f": {"HMC_SOBOL_NOI2F": 1},
+    "lb6": {"HMC_MIN_BLOCKS": 6},
+    "lb8": {"HMC_MIN_BLOCKS": 8},
+    "lb10": {"HMC_MIN_BLOCKS": 10},
+    "lb12": {"HMC_MIN_BLOCKS": 12},
 }
 
 
@@ -42,6 +45,9 @@ from paper_2309_10477_b200 import _lib, engine, greeks
 import bench
 p, spec, cfg = bench.workload()
 import os as _os, dataclasses as _dc
+if _os.environ.get("HMC_VARIANT_EURO"):
+    from paper_2309_10477_b200 import OptionSpec as _OS
+    spec = _OS("european", "call", 100.0, 1.0, 100.0)
 if _os.environ.get("HMC_VARIANT_SOBOL"):
     cfg = _dc.replace(cfg, sampler="sobol", sobol_highdim_ack=True, sobol_scramble=True, n_paths=2**22)
 job = engine.Job(p, spec, cfg, True)
