@@ -62,7 +62,10 @@ enum {
     HMC_E_INVALID = -1,   /* bad argument            -> ValidationError     */
     HMC_E_CUDA = -2,      /* CUDA runtime failure    -> DeviceError         */
     HMC_E_NODEVICE = -3,  /* no CUDA device visible  -> DeviceError         */
-    HMC_E_UNSUPPORTED = -4 /* e.g. Greeks for a put  -> UnsupportedProduct  */
+    HMC_E_UNSUPPORTED = -4, /* e.g. Greeks for a put -> UnsupportedProduct  */
+    HMC_E_BESSEL = -5,      /* exact scheme: Bessel series -> BesselNonConvergence */
+    HMC_E_QUAD = -6,        /* exact scheme: CF tail -> QuadratureNonConvergence   */
+    HMC_E_ROOT = -7         /* exact scheme: CDF inversion -> RootNotBracketed     */
 };
 
 enum { HMC_STYLE_EUROPEAN = 0, HMC_STYLE_ASIAN = 1 };
@@ -197,6 +200,19 @@ int hmc_surface_finalize(const hmc_model* model, const hmc_surface_spec* spec,
 /* Convenience: whole job on one device, synchronous, HOST output. */
 int hmc_surface(const hmc_model* model, const hmc_surface_spec* spec, const hmc_sim* sim,
                 double* h_out, int32_t device);
+
+/* Reference backend call exact_batch (_core.pyx:415-521): Broadie-Kaya
+ * exact paths stepping through step_times[0..n_steps] (step_times[0] = 0),
+ * fp64 on the GPU with the reference's random stream (3 main draws per step,
+ * Gamma substream derive(path_key, 1)) and algorithm.  avg_flags[n_steps]:
+ * 1 where the step's end is an averaging date.  uniforms: HOST
+ * (path_hi-path_lo, 3*n_steps) or NULL; out: HOST (path_hi-path_lo, 3)
+ * [s_T, avg, tw_sum].  Synchronous.  Numerical failures return
+ * HMC_E_BESSEL / HMC_E_QUAD / HMC_E_ROOT like the reference's exceptions. */
+int hmc_exact_batch_f64(const hmc_model* model, double s0, const double* step_times,
+                        int32_t n_steps, const int64_t* avg_flags, int64_t path_lo,
+                        int64_t path_hi, uint64_t key_run, const double* uniforms,
+                        double* out, int32_t device);
 
 /* Joe-Kuo direction numbers as used by scipy.stats.qmc.Sobol(scramble=False)
  * (30 bits): poly[dim], vinit[dim][18] from scipy's

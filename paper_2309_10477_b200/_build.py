@@ -28,6 +28,7 @@ UNITS = {
     "hmc_fast.cu": [],
     "hmc_replay.cu": ["-fmad=false"],
     "hmc_surface.cu": [],
+    "hmc_exact.cu": ["-fmad=false"],
 }
 
 

@@ -13,7 +13,8 @@ import ctypes
 import os
 import threading
 
-from .errors import DeviceError, UnsupportedProduct, ValidationError
+from .errors import (BesselNonConvergence, DeviceError, QuadratureNonConvergence,
+                     RootNotBracketed, UnsupportedProduct, ValidationError)
 
 LIB_PATH = os.environ.get("HMC_LIB_PATH") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "libhmc.so")
@@ -28,6 +29,7 @@ HMC_NW = 2 * HMC_NQ
 QUANTITIES = ("price", "delta", "rho", "gamma", "vega", "delta_fd", "rho_fd")
 
 HMC_OK, HMC_E_INVALID, HMC_E_CUDA, HMC_E_NODEVICE, HMC_E_UNSUPPORTED = 0, -1, -2, -3, -4
+HMC_E_BESSEL, HMC_E_QUAD, HMC_E_ROOT = -5, -6, -7
 STYLE = {"european": 0, "asian_arithmetic": 1}
 RIGHT = {"call": 0, "put": 1}
 SCHEME = {"euler": 1, "milstein": 2}
@@ -41,7 +43,7 @@ EXPORTS = (
     "hmc_reduce_chunks", "hmc_greeks", "hmc_discretised_batch_f64",
     "hmc_sobol_init_directions", "hmc_root_key", "hmc_derive_key", "hmc_philox_check",
     "hmc_surface_acc_words", "hmc_surface_workspace_bytes", "hmc_surface_partials",
-    "hmc_surface_finalize", "hmc_surface",
+    "hmc_surface_finalize", "hmc_surface", "hmc_exact_batch_f64",
 )
 HMC_SURF_MAX_STRIKES = 128
 HMC_SURF_MAX_MATS = 32
@@ -107,6 +109,8 @@ def _declare(L: ctypes.CDLL) -> None:
         "hmc_surface_finalize": (ctypes.c_int, [pM, ctypes.POINTER(SurfaceSpec), pS,
                                                 ctypes.POINTER(i64), pd]),
         "hmc_surface": (ctypes.c_int, [pM, ctypes.POINTER(SurfaceSpec), pS, pd, i32]),
+        "hmc_exact_batch_f64": (ctypes.c_int, [pM, dbl, pd, i32, ctypes.POINTER(i64), i64, i64, u64,
+                                               pd, pd, i32]),
         "hmc_root_key": (u64, [u64]),
         "hmc_derive_key": (u64, [u64, u64]),
     }
@@ -144,6 +148,12 @@ def check(rc: int) -> None:
         raise ValidationError(msg)
     if rc == HMC_E_UNSUPPORTED:
         raise UnsupportedProduct(msg)
+    if rc == HMC_E_BESSEL:
+        raise BesselNonConvergence(msg)
+    if rc == HMC_E_QUAD:
+        raise QuadratureNonConvergence(msg)
+    if rc == HMC_E_ROOT:
+        raise RootNotBracketed(msg)
     raise DeviceError(f"libhmc error {rc}: {msg}")
 
 

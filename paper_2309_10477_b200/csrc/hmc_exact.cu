@@ -1,0 +1,392 @@
+// hmc_exact.cu -- Broadie-Kaya exact simulation on sm_100a.
+//
+// The reference's exact scheme (_core.pyx:112-347, 415-521; exact.py;
+// ivlaw.py) one path per thread in fp64, same random stream, same algorithm:
+//   variance transition  v_t = c (Gamma(d/2 - 1/2, 2) + (Z + sqrt(lambda))^2)
+//                        Gamma by Marsaglia-Tsang on the path's gamma substream
+//   integrated variance  inverse of the Fourier-series CDF
+//                        F(x) = h x / pi + 2/pi sum_j sin(j h x)/j Re Phi(j h)
+//                        of the conditional characteristic function Phi
+//                        (modified Bessel series of complex argument), nodes
+//                        added until a tail criterion holds, second-order
+//                        Newton with bracketing and a bisection fallback
+//   log price            ln S += r dt - iv/2 + rho W2 + sqrt((1-rho^2) iv) Z3
+// Compiled with -fmad=false like the replay kernels.  Error codes follow
+// _core.pyx:36-40 and surface as BesselNonConvergence /
+// QuadratureNonConvergence / RootNotBracketed in Python.
+//
+// The reference caches Re Phi at up to MAX_NODES = 20000 nodes per call;
+// here the first kCacheNodes live in a per-thread slice of a device scratch
+// buffer (node-major, coalesced) and any further node is recomputed on the
+// fly -- identical values, bounded memory.  Typical node counts are 20-130.
+#include <cuda_runtime.h>
+
+#include "hmc_device.cuh"
+#include "hmc_launch.h"
+
+namespace hmc {
+
+namespace {
+
+constexpr int kMaxNodes = 20000;
+constexpr double kTailTol = 1e-7;
+constexpr int kTailRun = 3;
+constexpr double kNewtonTol = 1e-7;
+constexpr int kNewtonMaxIter = 100;
+constexpr int kBisectMaxIter = 200;
+constexpr double kPeriodStds = 12.0;
+constexpr double kDegenerateRelStd = 1e-5;
+constexpr double kPi = 3.14159265358979323846;
+
+struct cplx {
+    double re, im;
+};
+__device__ __forceinline__ cplx cx(double re, double im = 0.0) { return {re, im}; }
+__device__ __forceinline__ cplx operator+(cplx a, cplx b) { return {a.re + b.re, a.im + b.im}; }
+__device__ __forceinline__ cplx operator-(cplx a, cplx b) { return {a.re - b.re, a.im - b.im}; }
+__device__ __forceinline__ cplx operator*(cplx a, cplx b) {
+    return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re};
+}
+__device__ __forceinline__ cplx operator*(double s, cplx a) { return {s * a.re, s * a.im}; }
+__device__ __forceinline__ cplx operator/(cplx a, double s) { return {a.re / s, a.im / s}; }
+// Smith's algorithm (robust complex division)
+__device__ __forceinline__ cplx operator/(cplx a, cplx b) {
+    if (fabs(b.re) >= fabs(b.im)) {
+        const double r = b.im / b.re, d = b.re + b.im * r;
+        return {(a.re + a.im * r) / d, (a.im - a.re * r) / d};
+    }
+    const double r = b.re / b.im, d = b.re * r + b.im;
+    return {(a.re * r + a.im) / d, (a.im * r - a.re) / d};
+}
+__device__ __forceinline__ double cabs_(cplx a) { return hypot(a.re, a.im); }
+__device__ __forceinline__ cplx cexp_(cplx a) {
+    const double e = exp(a.re);
+    double s, c;
+    sincos(a.im, &s, &c);
+    return {e * c, e * s};
+}
+__device__ __forceinline__ cplx clog_(cplx a) { return {log(cabs_(a)), atan2(a.im, a.re)}; }
+// principal square root
+__device__ __forceinline__ cplx csqrt_(cplx a) {
+    if (a.re == 0.0 && a.im == 0.0) return {0.0, a.im};
+    const double t = sqrt(0.5 * (cabs_(a) + fabs(a.re)));
+    if (a.re >= 0.0) return {t, a.im / (2.0 * t)};
+    return {fabs(a.im) / (2.0 * t), copysign(t, a.im)};
+}
+
+enum { kErrNone = 0, kErrBesselRange = 1, kErrBesselConv = 2, kErrQuad = 3, kErrRoot = 4 };
+
+// power series of the modified Bessel function I_nu(z) / ((z/2)^nu / Gamma(nu+1))
+// (_core.pyx:143-159)
+__device__ cplx bessel_series(double nu, cplx z, int* err) {
+    if (cabs_(z) > 50.0) {
+        *err = kErrBesselRange;
+        return cx(0.0);
+    }
+    const cplx q = 0.25 * (z * z);
+    cplx term = cx(1.0), total = cx(1.0);
+    for (int k = 1; k <= 400; ++k) {
+        term = term * q / (k * (nu + k));
+        total = total + term;
+        if (cabs_(term) < 1e-12 * cabs_(total)) return total;
+    }
+    *err = kErrBesselConv;
+    return total;
+}
+
+// conditional characteristic function of the integrated variance (_core.pyx:162-188)
+__device__ cplx phi_eval(double kappa, double sigma2, double nu, double v_u, double v_t, double tau,
+                         double a, int* err) {
+    if (a == 0.0) return cx(1.0);
+    const cplx g = csqrt_(cx(kappa * kappa, -2.0 * sigma2 * a));
+    const double ek = exp(-kappa * tau);
+    const cplx eg = cexp_(cx(-g.re * tau, -g.im * tau));
+    const cplx one = cx(1.0);
+    const cplx lead = (g * cexp_(-0.5 * ((g - cx(kappa)) * cx(tau))) * cx(1.0 - ek)) /
+                      (cx(kappa) * (one - eg));
+    const cplx bracket = cx(kappa * (1.0 + ek) / (1.0 - ek)) - (g * (one + eg)) / (one - eg);
+    const cplx expo = cexp_(((v_u + v_t) / sigma2) * bracket);
+    const cplx egh = cexp_(-0.5 * (g * cx(tau)));
+    const cplx coeff_g = (4.0 * (g * egh)) / (cx(sigma2) * (one - egh * egh));
+    const double ekh = exp(-0.5 * kappa * tau);
+    const double coeff_k = 4.0 * kappa * ekh / (sigma2 * (1.0 - ekh * ekh));
+    const double w = sqrt(v_u * v_t);
+    const cplx log_q = clog_(g / kappa) - 0.5 * ((g - cx(kappa)) * cx(tau)) + cx(log(1.0 - ek)) -
+                       clog_(one - eg);
+    const cplx ratio = (cexp_(nu * log_q) * bessel_series(nu, w * coeff_g, err)) /
+                       bessel_series(nu, cx(w * coeff_k), err);
+    return lead * expo * ratio;
+}
+
+__device__ double ndtri_d(double u) {
+    double q, s, num, den, x, e, corr, p, sign;
+    if (u < 1e-300) u = 1e-300;
+    if (u > 1.0 - 1e-16) u = 1.0 - 1e-16;
+    if (0.02425 <= u && u <= 0.97575) {
+        q = u - 0.5;
+        s = q * q;
+        num = ((((-3.969683028665376e+01 * s + 2.209460984245205e+02) * s - 2.759285104469687e+02) * s +
+                1.383577518672690e+02) * s - 3.066479806614716e+01) * s + 2.506628277459239e+00;
+        den = ((((-5.447609879822406e+01 * s + 1.615858368580409e+02) * s - 1.556989798598866e+02) * s +
+                6.680131188771972e+01) * s - 1.328068155288572e+01) * s + 1.0;
+        x = q * num / den;
+    } else {
+        if (u < 0.02425) {
+            p = u;
+            sign = 1.0;
+        } else {
+            p = 1.0 - u;
+            sign = -1.0;
+        }
+        q = sqrt(-2.0 * log(p));
+        num = ((((-7.784894002430293e-03 * q - 3.223964580411365e-01) * q - 2.400758277161838e+00) * q -
+                2.549732539343734e+00) * q + 4.374664141464968e+00) * q + 2.938163982698783e+00;
+        den = (((7.784695709041462e-03 * q + 3.224671290700398e-01) * q + 2.445134137142996e+00) * q +
+               3.754408661907416e+00) * q + 1.0;
+        x = sign * num / den;
+    }
+    e = 0.5 * erfc(-x / sqrt(2.0)) - u;
+    corr = e * 2.5066282746310002 * exp(0.5 * x * x);
+    x -= corr / (1.0 + 0.5 * x * corr);
+    return x;
+}
+
+// Marsaglia-Tsang on the reference stream (_core.pyx:116-136)
+__device__ double sample_gamma(unsigned long long key, double shape, double scale) {
+    double boost = 1.0, alpha = shape;
+    unsigned long long ctr = 0;
+    if (alpha < 1.0) {
+        boost = pow(uniform_at(key, 0), 1.0 / alpha);
+        alpha += 1.0;
+        ctr = 1;
+    }
+    const double d = alpha - 1.0 / 3.0;
+    const double c = 1.0 / sqrt(9.0 * d);
+    while (true) {
+        const double x = ndtri_d(uniform_at(key, ctr));
+        double u = uniform_at(key, ctr + 1);
+        ctr += 2;
+        double v = 1.0 + c * x;
+        if (v <= 0.0) continue;
+        v = v * v * v;
+        if (u < 1e-300) u = 1e-300;
+        if (log(u) < 0.5 * x * x + d - d * v + d * log(v)) return boost * d * v * scale;
+    }
+}
+
+struct NodeCache {
+    double* base;  // scratch + thread slot; node j at base[j * stride]
+    long long stride;
+    int cap;
+    // for recomputation past the cache
+    double kappa, sigma2, nu, v_u, v_t, tau, h;
+    __device__ double re(int j, int* err) const {  // j 0-based
+        if (j < cap) return base[(size_t)j * stride];
+        return phi_eval(kappa, sigma2, nu, v_u, v_t, tau, (j + 1) * h, err).re;
+    }
+};
+
+__device__ double cdf_at(double x, double h, int n, const NodeCache& nc, int* err) {
+    double f = h * x / kPi;
+    for (int j = 1; j <= n; ++j) f += (2.0 / kPi) * sin(j * h * x) / j * nc.re(j - 1, err);
+    return f;
+}
+
+__device__ double bisect_iv(double u, double lo, double hi, double h, int n, const NodeCache& nc,
+                            int* err) {
+    const double f_hi = cdf_at(hi, h, n, nc, err);
+    if (f_hi < u - kNewtonTol) {
+        if (f_hi < u - 1e-4) {
+            *err = kErrRoot;
+            return 0.0;
+        }
+        return hi;
+    }
+    double x = 0.5 * (lo + hi);
+    for (int it = 0; it < kBisectMaxIter; ++it) {
+        const double f = cdf_at(x, h, n, nc, err);
+        if (fabs(f - u) < kNewtonTol) return x;
+        if (f > u)
+            hi = x;
+        else
+            lo = x;
+        x = 0.5 * (lo + hi);
+        if (hi - lo < 1e-16 * (1.0 + hi)) break;
+    }
+    if (fabs(cdf_at(x, h, n, nc, err) - u) < 1e-6) return x;
+    *err = kErrRoot;
+    return 0.0;
+}
+
+// inverse-CDF draw of the conditional integrated variance (_core.pyx:195-310)
+__device__ double sample_iv(double kappa, double theta, double sigma, double dof, double v_u,
+                            double v_t, double dt, double u, NodeCache& nc, int* err) {
+    const double sigma2 = sigma * sigma;
+    const double nu = 0.5 * dof - 1.0;
+    if (u < 1e-12) u = 1e-12;
+    if (u > 1.0 - 1e-12) u = 1.0 - 1e-12;
+    if (sigma < 1e-4 * kappa) return theta * dt + (v_u - theta) * (1.0 - exp(-kappa * dt)) / kappa;
+
+    double scale = 0.5 * (v_u + v_t);
+    if (scale < 0.01 * theta) scale = 0.01 * theta;
+    scale *= dt;
+    double m1 = scale, eps;
+    cplx phi;
+    for (int it = 0; it < 2; ++it) {
+        eps = 0.05 / m1;
+        phi = phi_eval(kappa, sigma2, nu, v_u, v_t, dt, eps, err);
+        const double m1_new = phi.im / eps;
+        if (!(m1_new > 0.0) || !isfinite(m1_new)) break;
+        m1 = m1_new;
+    }
+    eps = 0.05 / m1;
+    phi = phi_eval(kappa, sigma2, nu, v_u, v_t, dt, eps, err);
+    m1 = phi.im / eps;
+    const double m2 = -2.0 * (phi.re - 1.0) / (eps * eps);
+    double var = m2 - m1 * m1;
+    if (var < 0.0) var = 0.0;
+    const double mean = m1, std = sqrt(var);
+    if (*err != kErrNone) return 0.0;
+    if (std < kDegenerateRelStd * mean) {
+        const double r = mean + std * ndtri_d(u);
+        return r > 0.0 ? r : 0.0;
+    }
+    const double h = 2.0 * kPi / (mean + kPeriodStds * std);
+    nc.kappa = kappa;
+    nc.sigma2 = sigma2;
+    nc.nu = nu;
+    nc.v_u = v_u;
+    nc.v_t = v_t;
+    nc.tau = dt;
+    nc.h = h;
+
+    int n = 0, run = 0;
+    while (run < kTailRun) {
+        if (n >= kMaxNodes) {
+            *err = kErrQuad;
+            return 0.0;
+        }
+        const int j = n + 1;
+        const cplx p = phi_eval(kappa, sigma2, nu, v_u, v_t, dt, j * h, err);
+        if (*err != kErrNone) return 0.0;
+        if (n < nc.cap) nc.base[(size_t)n * nc.stride] = p.re;
+        const double mag = (2.0 / kPi) * cabs_(p) / j;
+        if (mag < kTailTol)
+            ++run;
+        else
+            run = 0;
+        ++n;
+    }
+
+    double lo = 0.0, hi = 2.0 * kPi / h, x = mean;
+    if (x < 1e-3 * hi) x = 1e-3 * hi;
+    if (x > 0.9 * hi) x = 0.9 * hi;
+    for (int it = 0; it < kNewtonMaxIter; ++it) {
+        double f = h * x / kPi, d1 = h / kPi, d2 = 0.0;
+        for (int j = 1; j <= n; ++j) {
+            const double s_j = j * h;
+            const double rp = nc.re(j - 1, err);
+            const double sx = sin(s_j * x), cxv = cos(s_j * x);
+            f += (2.0 / kPi) * sx / j * rp;
+            d1 += (2.0 * h / kPi) * cxv * rp;
+            d2 -= (2.0 * h / kPi) * s_j * sx * rp;
+        }
+        const double efun = f - u;
+        if (fabs(efun) < kNewtonTol) return x;
+        if (efun > 0.0) {
+            if (x < hi) hi = x;
+        } else {
+            if (x > lo) lo = x;
+        }
+        bool have_step = false;
+        double step = 0.0;
+        if (d1 > 0.0) {
+            const double disc = 1.0 - 2.0 * efun * d2 / (d1 * d1);
+            if (fabs(d2) < 1e-300 || fabs(2.0 * efun * d2) < 1e-12 * d1 * d1) {
+                step = -efun / d1;
+                have_step = true;
+            } else if (disc > 0.0) {
+                step = -(d1 / d2) * (1.0 - sqrt(disc));
+                have_step = true;
+            }
+        }
+        if (!have_step || x + step <= lo || x + step >= hi)
+            x = 0.5 * (lo + hi);
+        else
+            x = x + step;
+    }
+    return bisect_iv(u, lo, hi, h, n, nc, err);
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kExactThreads) exact_batch_kernel(const ExactArgs e) {
+    const long long n = e.path_hi - e.path_lo;
+    const long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    NodeCache nc{};
+    nc.base = e.scratch + slot;
+    nc.stride = stride;
+    nc.cap = kExactCacheNodes;
+    const bool point_mass = e.sigma < 1e-4 * e.kappa;
+    for (long long i = slot; i < n; i += stride) {
+        int err = kErrNone;
+        const unsigned long long key_path = derive(e.key_run, (unsigned long long)(e.path_lo + i));
+        const unsigned long long main_key = derive(key_path, 0ULL);
+        const unsigned long long gamma_root = derive(key_path, 1ULL);
+        double ln_s = log(e.s0), v = e.v0, price_sum = 0.0, tw_sum = 0.0;
+        const double* urow = e.uniforms ? e.uniforms + (size_t)i * 3 * e.n_steps : nullptr;
+        for (int k = 0; k < e.n_steps; ++k) {
+            const double dt = e.times[k + 1] - e.times[k];
+            double u1, u2, u3;
+            if (urow) {
+                u1 = urow[3 * k];
+                u2 = urow[3 * k + 1];
+                u3 = urow[3 * k + 2];
+            } else {
+                u1 = uniform_at(main_key, (unsigned long long)(3 * k));
+                u2 = uniform_at(main_key, (unsigned long long)(3 * k + 1));
+                u3 = uniform_at(main_key, (unsigned long long)(3 * k + 2));
+            }
+            const double ek = exp(-e.kappa * dt);
+            const double c = e.sigma * e.sigma * (1.0 - ek) / (4.0 * e.kappa);
+            const double lam = 4.0 * e.kappa * ek * v / (e.sigma * e.sigma * (1.0 - ek));
+            const double z1 = ndtri_d(u1);
+            const double g = sample_gamma(derive(gamma_root, (unsigned long long)k), 0.5 * (e.dof - 1.0), 2.0);
+            const double shifted = z1 + sqrt(lam);
+            const double v_new = c * (g + shifted * shifted);
+            const double iv = sample_iv(e.kappa, e.theta, e.sigma, e.dof, v, v_new, dt, u2, nc, &err);
+            if (err != kErrNone) break;
+            double int_w2;
+            if (point_mass)
+                int_w2 = sqrt(iv) * ndtri_d(u2);
+            else
+                int_w2 = (v_new - v - e.kappa * e.theta * dt + e.kappa * iv) / e.sigma;
+            const double z3 = ndtri_d(u3);
+            double var_ln = (1.0 - e.rho * e.rho) * iv;
+            if (var_ln < 0.0) var_ln = 0.0;
+            ln_s = ln_s + e.r * dt - 0.5 * iv + e.rho * int_w2 + sqrt(var_ln) * z3;
+            v = v_new;
+            if (e.flags[k]) {
+                const double s_now = exp(ln_s);
+                price_sum += s_now;
+                tw_sum += s_now * e.times[k + 1];
+            }
+        }
+        if (err != kErrNone) {
+            atomicMax(e.err_flag, err);
+            e.out[3 * i] = e.out[3 * i + 1] = e.out[3 * i + 2] = 0.0;
+            continue;
+        }
+        e.out[3 * i + 0] = exp(ln_s);
+        e.out[3 * i + 1] = price_sum / e.n_dates;
+        e.out[3 * i + 2] = tw_sum / e.n_dates;
+    }
+}
+
+cudaError_t launch_exact(const ExactArgs& e, int grid, cudaStream_t s) {
+    exact_batch_kernel<<<grid, kExactThreads, 0, s>>>(e);
+    return cudaGetLastError();
+}
+
+}  // namespace hmc

@@ -56,6 +56,26 @@ struct SurfArgs {
 cudaError_t launch_surface(const KernelArgs& a, const SurfArgs& s, long long n_tiles, int grid_x,
                            cudaStream_t stream);
 
+// ---- Broadie-Kaya exact simulation (hmc_exact.cu) --------------------------
+constexpr int kExactThreads = 128;
+constexpr int kExactCacheNodes = 256;  // Re Phi nodes cached per thread (rest recomputed)
+
+struct ExactArgs {
+    double kappa, theta, sigma, rho, r, v0, dof, s0;
+    const double* times;     // [n_steps + 1] step endpoints, times[0] = 0
+    const long long* flags;  // [n_steps] 1 if the step's end is an averaging date
+    int n_steps;
+    long long n_dates;
+    long long path_lo, path_hi;
+    unsigned long long key_run;
+    const double* uniforms;  // [n][3 n_steps] or null
+    double* out;             // [n][3]
+    double* scratch;         // [kExactCacheNodes][grid threads]
+    int* err_flag;           // max reference error code seen
+};
+
+cudaError_t launch_exact(const ExactArgs& e, int grid, cudaStream_t s);
+
 // fp32 production kernel (hmc_fast.cu): tiles[run][tile][HMC_NW]
 cudaError_t launch_fast_greeks(const KernelArgs& a, double* d_tiles, long long n_tiles,
                                cudaStream_t s);

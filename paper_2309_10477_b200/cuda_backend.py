@@ -7,6 +7,9 @@ reference signatures.  The reference engine can be driven through it
 unchanged, e.g. ``monkeypatch.setattr(engine, "get_backend", lambda:
 cuda_backend)`` (the swap ``tests/test_backends.py:63-71`` uses).
 
+``exact_batch`` runs the reference's Broadie-Kaya scheme (same stream, same
+algorithm) on the GPU in fp64.
+
 ``discretised_batch`` is the fp64 replay kernel: the reference's SplitMix64
 stream (or the caller's uniforms), its Acklam+Halley inverse normal and its
 operation order, one path per GPU thread; per-path outputs match the
@@ -20,7 +23,6 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from .errors import UnsupportedProduct
 
 BACKEND_NAME = "cuda"
 
@@ -62,8 +64,32 @@ def discretised_batch(params, s0: float, T: float, n_steps: int, milstein: bool,
     return out
 
 
-def exact_batch(params, s0, step_times, avg_flags, path_lo, path_hi, key_run, uniforms):
-    """Broadie-Kaya exact simulation is out of the GPU scope."""
-    raise UnsupportedProduct(
-        "exact (Broadie-Kaya) simulation is not served by the cuda backend; "
-        "it remains the reference's CPU baseline")
+def exact_batch(params, s0: float, step_times, avg_flags, path_lo: int, path_hi: int,
+                key_run: int, uniforms) -> np.ndarray:
+    """Broadie-Kaya exact paths stepping through ``step_times`` (reference
+    ``_core.pyx:415-521``), fp64 on the GPU with the reference's stream and
+    algorithm: (n, 3) float64 [s_T, avg, tw_sum].  Numerical failures raise
+    the reference's exceptions (BesselNonConvergence, ...)."""
+    times = np.ascontiguousarray(step_times, dtype=np.float64)
+    flags = np.ascontiguousarray(avg_flags, dtype=np.int64)
+    n_steps = times.size - 1
+    if flags.size != n_steps:
+        raise ValueError("avg_flags needs one flag per step")
+    n = int(path_hi) - int(path_lo)
+    out = np.empty((max(n, 0), 3))
+    u = None
+    if uniforms is not None:
+        u = np.ascontiguousarray(uniforms, dtype=np.float64)
+        if u.shape[0] < n or u.shape[1] < 3 * n_steps:
+            raise ValueError("uniforms must be at least (path_hi - path_lo, 3 * n_steps)")
+        if u.shape[1] != 3 * n_steps:
+            u = np.ascontiguousarray(u[:, : 3 * n_steps])
+    m = _lib.Model(params.kappa, params.theta, params.sigma, params.rho, params.r, params.v0)
+    pd = ctypes.POINTER(ctypes.c_double)
+    rc = _lib.lib().hmc_exact_batch_f64(
+        ctypes.byref(m), float(s0), times.ctypes.data_as(pd), n_steps,
+        flags.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), int(path_lo), int(path_hi),
+        int(key_run) & (2**64 - 1), None if u is None else u.ctypes.data_as(pd),
+        out.ctypes.data_as(pd), _device())
+    _lib.check(rc)
+    return out

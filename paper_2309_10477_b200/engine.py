@@ -49,9 +49,7 @@ def _validate(spec: OptionSpec, config: SimConfig, want_greeks: bool) -> list[in
     if want_greeks and spec.right != "call":
         raise UnsupportedProduct("pathwise Greeks are derived for calls only")
     if config.scheme == "exact":
-        raise UnsupportedProduct(
-            "the exact (Broadie-Kaya) scheme is the reference's CPU baseline and "
-            "is not served by the GPU engine; use scheme='milstein' or 'euler'")
+        return []
     grid = GridSpec(maturity=spec.maturity, n_steps=config.n_steps)
     if spec.is_asian:
         return averaging_indices(grid, spec.averaging_times)
@@ -158,9 +156,14 @@ def summarise(config: SimConfig, sums: np.ndarray, wall_ms: float,
 
 def _execute(params: HestonParams, spec: OptionSpec, config: SimConfig,
              want_greeks: bool, group=None) -> dict[str, McSummary]:
-    job = Job(params, spec, config, want_greeks)
     t0 = time.perf_counter()
-    sums = job.run_device(group)
+    if config.scheme == "exact":
+        from . import exact
+        _validate(spec, config, want_greeks)
+        sums = exact.execute(params, spec, config, want_greeks,
+                             bump_sizes(params, spec, config), group)
+    else:
+        sums = Job(params, spec, config, want_greeks).run_device(group)
     wall = (time.perf_counter() - t0) * 1000.0 / config.n_runs
     res = summarise(config, sums, wall)
     if not want_greeks:

@@ -106,6 +106,34 @@ def replay_cases(hm, core):
     print(f"replay_cases.npz: {len(cases)} cases")
 
 
+def exact_cases(hm, core):
+    """Reference exact_batch (Broadie-Kaya) outputs (_core.pyx:415-521)."""
+    from hestonmc.model import DEFAULT_PARAMS, HestonParams
+    from hestonmc.rng import derive_key, root_key, sobol_points
+    kr = lambda seed, run=0: int(derive_key(root_key(seed), run))  # noqa: E731
+    cases = {
+        "paper_euro_1": (DEFAULT_PARAMS, 100.0, [0.0, 1.0], [1], 0, 96, kr(42), None),
+        "paper_asian_4": (DEFAULT_PARAMS, 100.0, [0.0, 0.25, 0.5, 0.75, 1.0], [1, 1, 1, 1], 5, 69,
+                          kr(7, 2), None),
+        "bench_euro_1": (BENCH, 100.0, [0.0, 1.0], [1], 1000, 1064, kr(3), None),
+        "bench_half_2": (BENCH, 95.0, [0.0, 0.25, 0.5], [0, 1], 0, 64, kr(11), None),
+        "paper_sobol_1": (DEFAULT_PARAMS, 100.0, [0.0, 1.0], [1], 0, 64, kr(42),
+                          sobol_points(3, 1, 64)),
+    }
+    out, meta = {}, {}
+    for name, (p, s0, times, flags, lo, hi, k, uu) in cases.items():
+        res = core.exact_batch(HestonParams(**p), s0, np.array(times), np.array(flags, dtype=np.int64),
+                               lo, hi, k, uu)
+        out[f"{name}__out"] = res
+        if uu is not None:
+            out[f"{name}__uniforms"] = uu
+        meta[name] = dict(params=p, s0=s0, times=times, flags=flags, path_lo=lo, path_hi=hi,
+                          key_run=str(k), has_uniforms=uu is not None)
+    out["__meta__"] = np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8)
+    np.savez_compressed(os.path.join(HERE, "exact_cases.npz"), **out)
+    print(f"exact_cases.npz: {len(cases)} cases")
+
+
 def _bump_spot(spec, h):
     from hestonmc.model import OptionSpec
     return OptionSpec(style=spec.style, right=spec.right, strike=spec.strike,
@@ -143,6 +171,12 @@ def engine_cases(hm):
         ("paper_asian_sobol", paper, asian4, dict(scheme="milstein", sampler="sobol", sobol_highdim_ack=True,
                                                   n_paths=1000, n_steps=16, n_runs=3, seed=3)),
         ("bench_put_price", bench, put, dict(scheme="milstein", n_paths=3000, n_steps=32, n_runs=2, seed=5)),
+        # Broadie-Kaya exact scheme (the reference's default), cf. tests/test_backends.py:63-71
+        ("paper_euro_exact_sobol", paper, euro, dict(scheme="exact", sampler="sobol", n_paths=256,
+                                                     n_steps=1, n_runs=2, seed=3)),
+        ("paper_euro_exact", paper, euro, dict(scheme="exact", n_paths=5000, n_steps=1, n_runs=2, seed=42)),
+        ("paper_asian_exact", paper, asian4, dict(scheme="exact", sampler="sobol", n_paths=700,
+                                                  n_steps=4, n_runs=2, seed=42)),
     ]
     h_s, h_r, h_v = 0.005, 1e-4, 0.01
     out = {}
@@ -294,6 +328,7 @@ def main():
     engine_cases(hm)
     rng_cases(hm)
     sobol_cases(hm)
+    exact_cases(hm, core)
     if args.stats:
         stats_golden(hm, core)
 

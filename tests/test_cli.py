@@ -9,7 +9,7 @@ import pytest
 from paper_2309_10477_b200 import cli
 from paper_2309_10477_b200.cli import CSV_HEADER, main, parse_config
 
-FAST = ["--paths", "4096", "--runs", "2", "--steps", "16"]
+FAST = ["--paths", "4096", "--runs", "2", "--steps", "16", "--scheme", "milstein"]
 
 
 def run(capsys, argv):
@@ -24,7 +24,7 @@ class TestParsing:
         p = man.params
         assert (p.kappa, p.theta, p.sigma, p.v0, p.r) == (6.21, 0.019, 0.61, 0.010201, 0.0319)
         assert man.spec.strike == man.spec.spot == 100.0 and man.spec.maturity == 1.0
-        assert man.config.scheme == "milstein" and man.config.precision == "fp32"
+        assert man.config.scheme == "exact" and man.config.precision == "fp32"  # reference default
 
     def test_asian_dates(self):
         _, man, _ = parse_config(["price", "--product", "asian", "--averaging-times",
@@ -69,11 +69,11 @@ class TestUsageErrors:
     @pytest.mark.parametrize("argv,needle", [
         (["price", "--rho", "1.5"], "rho"),
         (["price", "--paths", "0"], "n_paths"),
-        (["price", "--sampler", "sobol"], "sobol"),
+        (["price", "--scheme", "milstein", "--sampler", "sobol"], "sobol"),
         (["greeks", "--right", "put"], "call"),
-        (["price", "--scheme", "exact"], "exact"),
         (["bench", "--scheme", "heun"], "heun"),
-        (["price", "--product", "asian", "--averaging-times", "0.3", "--steps", "16"], "grid"),
+        (["price", "--scheme", "milstein", "--product", "asian", "--averaging-times", "0.3",
+          "--steps", "16"], "grid"),
     ])
     def test_exit_code_2(self, capsys, argv, needle):
         code, _, err = run(capsys, argv)
@@ -106,6 +106,11 @@ class TestOutputs:
         names = [ln.split(",")[0] for ln in lines[1:]]
         assert names == ["price", "delta", "gamma", "vega", "rho", "delta_fd", "rho_fd"]
 
+    def test_exact_default_scheme(self, capsys):
+        # the reference's default invocation: exact scheme, sobol, 256 paths
+        code, out, _ = run(capsys, ["price", "--paths", "256", "--runs", "2", "--sampler", "sobol"])
+        assert code == 0 and "price" in out
+
     def test_jsonl(self, capsys):
         code, out, _ = run(capsys, ["price", "--format", "jsonl", "--precision", "fp64"] + FAST)
         row = json.loads(out.strip().splitlines()[0])
@@ -114,7 +119,8 @@ class TestOutputs:
 
     def test_surface_csv(self, capsys):
         code, out, _ = run(capsys, ["surface", "--strikes", "90:111:10", "--maturities", "0.5,1",
-                                    "--steps", "32", "--paths", "8192", "--runs", "2", "--s0", "100"])
+                                    "--steps", "32", "--paths", "8192", "--runs", "2", "--s0", "100",
+                                    "--scheme", "milstein"])
         lines = out.strip().splitlines()
         assert code == 0 and lines[0].startswith("style,maturity,strike,quantity")
         assert len(lines) == 1 + 2 * 7 * 2 * 3

@@ -98,9 +98,6 @@ class TestEngineValidation:
         with pytest.raises(UnsupportedProduct):
             engine.greeks(params, put, SimConfig(scheme="milstein"))
 
-    def test_exact_scheme_not_served(self, params, euro_call):
-        with pytest.raises(UnsupportedProduct):
-            engine.price(params, euro_call, SimConfig(scheme="exact"))
 
     def test_off_grid_asian_date_rejected(self, params):
         spec = OptionSpec(style="asian_arithmetic", right="call", strike=100.0, maturity=1.0,
@@ -131,6 +128,6 @@ class TestSurfaceValidation:
         with pytest.raises(ValidationError):
             surface(params, list(range(1, 200)), [1.0], cfg)     # > 128 strikes
         with pytest.raises(UnsupportedProduct):
-            surface(params, [100.0], [1.0], SimConfig(scheme="exact"))
+            surface(params, [100.0], [1.0], SimConfig(scheme="exact", n_steps=1))
         with pytest.raises(UnsupportedProduct):
             surface(params, [100.0], [1.0], SimConfig(scheme="milstein", precision="fp64"))
