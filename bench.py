@@ -72,6 +72,9 @@ def secondary_workloads(reps: int = 3) -> dict:
                                                sobol_highdim_ack=True, sobol_scramble=True,
                                                n_paths=2**22, n_steps=252, n_runs=1, seed=7)),
             2**22 * 252),
+        "exact_bk_european_price_2^17": (
+            lambda: greeks(p, euro, SimConfig(scheme="exact", n_paths=2**17, n_steps=1, n_runs=1,
+                                              seed=7)), 2**17),
         "c5_surface_64Kx8T_euro+asian_full_greeks_2^22x504": (
             lambda: surface(p, np.arange(70.0, 134.0, 1.0), [0.25 * i for i in range(1, 9)],
                             SimConfig(scheme="milstein", n_paths=2**22, n_steps=504, n_runs=1,
@@ -91,6 +94,28 @@ def secondary_workloads(reps: int = 3) -> dict:
         ms = sorted(ts)[len(ts) // 2]
         out[name] = {"ms": ms, "path_steps_per_s": path_steps / (ms / 1e3)}
     return out
+
+
+def cpu_exact_block(n_paths: int = 2 ** 13) -> dict:
+    """The reference's own Broadie-Kaya kernel (oracle/_ref) on all host
+    cores, European, one [0, T] step, 4096-path jobs as engine.py."""
+    import oracle
+    from concurrent.futures import ThreadPoolExecutor
+    import numpy as np
+    from paper_2309_10477_b200 import BENCH_PARAMS, HestonParams
+    core = oracle.ref_core()
+    if core is None:
+        return {"value": None}
+    p = HestonParams(**BENCH_PARAMS)
+    workers = os.cpu_count() or 1
+    jobs = [(lo, min(lo + 512, n_paths)) for lo in range(0, n_paths, 512)]
+    times, flags = np.array([0.0, 1.0]), np.array([1], dtype=np.int64)
+    with ThreadPoolExecutor(workers) as pool:
+        t0 = time.perf_counter()
+        list(pool.map(lambda j: core.exact_batch(p, 100.0, times, flags, j[0], j[1], 7, None), jobs))
+        secs = time.perf_counter() - t0
+    return {"value": n_paths / secs, "unit": "paths/s", "cores": workers, "kind": "reference",
+            "sample": f"{n_paths} European Broadie-Kaya paths (1 step), 512-path jobs"}
 
 
 def config_block(n_gpus: int) -> dict:
@@ -347,6 +372,8 @@ def run_b200(args) -> None:
             line["cpu_baseline"] = cpu_baseline_block()
         if world == 1 and not args.no_e2e:
             line["secondary"] = secondary_workloads()
+            if not args.no_cpu:
+                line["cpu_baseline_exact"] = cpu_exact_block()
         print(json.dumps(line))
     if distributed:
         dist.destroy_process_group()
