@@ -115,7 +115,8 @@ class Job:
             keep.append(v)
             self.sim.sobol_v = ctypes.cast(ctypes.c_void_p(v.data_ptr()), ctypes.POINTER(ctypes.c_uint32))
             self.sim.sobol_v_on_device = 1
-        local = torch.zeros((self.n_runs, sl.n_chunks, _lib.HMC_NW), dtype=torch.float64, device=dev)
+        # every chunk of the slice is written by hmc_greeks_chunks
+        local = torch.empty((self.n_runs, sl.n_chunks, _lib.HMC_NW), dtype=torch.float64, device=dev)
         if sl.n_paths > 0:
             self.sim.path_lo, self.sim.path_hi = sl.path_lo, sl.path_hi
             work = torch.empty(int(L.hmc_workspace_bytes(ctypes.byref(self.sim))),
@@ -139,19 +140,20 @@ def summarise(config: SimConfig, sums: np.ndarray, wall_ms: float,
               names=_QNAMES) -> dict[str, McSummary]:
     """Reference ``_summaries`` (``engine.py:128-139``) plus per-path SE.
     ``sums`` is [n_runs, HMC_NW] = {sum, sum of squares} per quantity."""
-    out = {}
-    N = config.n_paths
-    M = config.n_runs * N
-    for q, name in enumerate(names):
-        runs = sums[:, 2 * q] / N
-        sd = float(np.std(runs, ddof=1)) if config.n_runs > 1 else 0.0
-        s, ss = float(sums[:, 2 * q].sum()), float(sums[:, 2 * q + 1].sum())
-        var = max(ss - s * s / M, 0.0) / (M - 1) if M > 1 else 0.0
-        out[name] = McSummary(estimate=float(np.mean(runs)), std_error=sd,
-                              per_run_values=[float(x) for x in runs], wall_ms=wall_ms,
-                              n_paths=N, n_runs=config.n_runs,
-                              path_std_error=math.sqrt(var / M))
-    return out
+    N, R = config.n_paths, config.n_runs
+    M = R * N
+    # one row per quantity, contiguous: the row reductions are exactly the
+    # reference's 1-D np.mean / np.std per quantity (engine.py:133-135)
+    runs = np.ascontiguousarray(sums[:, 0::2].T) / N
+    est = np.mean(runs, axis=1)
+    sd = np.std(runs, axis=1, ddof=1) if R > 1 else np.zeros(len(names))
+    s, ss = sums[:, 0::2].sum(axis=0), sums[:, 1::2].sum(axis=0)
+    var = np.maximum(ss - s * s / M, 0.0) / (M - 1) if M > 1 else np.zeros(len(names))
+    pse = np.sqrt(var / M)
+    runs_l, est_l, sd_l, pse_l = runs.tolist(), est.tolist(), sd.tolist(), pse.tolist()
+    return {name: McSummary(estimate=est_l[q], std_error=sd_l[q], per_run_values=runs_l[q],
+                            wall_ms=wall_ms, n_paths=N, n_runs=R, path_std_error=pse_l[q])
+            for q, name in enumerate(names)}
 
 
 def _execute(params: HestonParams, spec: OptionSpec, config: SimConfig,

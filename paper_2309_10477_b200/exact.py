@@ -94,7 +94,10 @@ def execute(params: HestonParams, spec: OptionSpec, config: SimConfig, want_gree
         key_run = _lib.lib().hmc_derive_key(key_root, run)
         u = None
         if config.sampler == "sobol":  # engine.py:97-101
-            u = sobol.points(3 * n_steps, 1 + run * config.n_paths + sl.path_lo, sl.n_paths)
+            if config.sobol_scramble:      # randomised QMC: points 1..N, per-run shifts
+                u = sobol.points(3 * n_steps, 1 + sl.path_lo, sl.n_paths, key_run=key_run)
+            else:
+                u = sobol.points(3 * n_steps, 1 + run * config.n_paths + sl.path_lo, sl.n_paths)
         partials = np.zeros((len(jobs), 14))
         if sl.n_paths > 0:
             obs = cuda_backend.exact_batch(params, spec.spot, times, flags, sl.path_lo, sl.path_hi,

@@ -49,9 +49,27 @@ def directions(dim: int) -> np.ndarray:
     return out
 
 
-def points(dim: int, start: int, count: int) -> np.ndarray:
+def _mix64(z: np.ndarray) -> np.ndarray:
+    with np.errstate(over="ignore"):
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
+
+
+def digital_shifts(key_run: int, dim: int) -> np.ndarray:
+    """Per-dimension 30-bit random digital shifts of one run -- the same
+    values as the kernels' ``sobol_shift`` (csrc/hmc_device.cuh)."""
+    d = np.arange(1, dim + 1, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = np.uint64(key_run & (2**64 - 1)) ^ (d * np.uint64(0x9E3779B97F4A7C15))
+    return _mix64(z) >> np.uint64(34)
+
+
+def points(dim: int, start: int, count: int, key_run: int | None = None) -> np.ndarray:
     """Host evaluation of rows start..start+count-1 (float64, as scipy's
-    ``random``) from the same table the kernels use -- for checks."""
+    ``random``) from the same table the kernels use.  With ``key_run`` the
+    run's digital shifts are applied and cell midpoints returned (the
+    randomised-QMC points of ``SimConfig(sobol_scramble=True)``)."""
     v = directions(dim).astype(np.uint64)
     n = np.arange(start, start + count, dtype=np.uint64)
     g = n ^ (n >> np.uint64(1))
@@ -59,4 +77,7 @@ def points(dim: int, start: int, count: int) -> np.ndarray:
     for b in range(BITS):
         on = ((g >> np.uint64(b)) & np.uint64(1)).astype(bool)
         x[on] ^= v[b]
-    return x.astype(np.float64) * 2.0 ** -BITS
+    if key_run is None:
+        return x.astype(np.float64) * 2.0 ** -BITS
+    x ^= digital_shifts(key_run, dim)[None, :]
+    return (x.astype(np.float64) + 0.5) * 2.0 ** -BITS

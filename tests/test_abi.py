@@ -125,3 +125,15 @@ def test_no_cpu_fallback_without_device():
     from paper_2309_10477_b200 import cuda_backend
     with pytest.raises(DeviceError):
         cuda_backend.discretised_batch(p, 100.0, 1.0, 8, True, 0, 16, 1, None, np.array([8]))
+
+
+def test_host_digital_shifts_match_device_derivation():
+    """sobol.digital_shifts restates csrc sobol_shift: mix64(key ^ (d+1) GOLDEN) >> 34."""
+    import oracle
+    key = 0x0123456789ABCDEF
+    got = sobol.digital_shifts(key, 6)
+    for d in range(6):
+        want = oracle.mix64(key ^ (((d + 1) * 0x9E3779B97F4A7C15) & (2**64 - 1))) >> 34
+        assert int(got[d]) == want
+    pts = sobol.points(4, 1, 8, key_run=key)
+    assert np.all((pts > 0) & (pts < 1))
