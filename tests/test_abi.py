@@ -77,7 +77,7 @@ def test_slice_geometry():
 
 @pytest.mark.parametrize("over,code", [
     (dict(right=1), _lib.HMC_E_UNSUPPORTED),          # put Greeks (engine.py:120-121)
-    (dict(scheme=0), _lib.HMC_E_UNSUPPORTED),         # exact scheme is CPU-only
+    (dict(scheme=0), _lib.HMC_E_UNSUPPORTED),         # exact scheme: hmc_exact_batch_f64
     (dict(path_lo=5), _lib.HMC_E_INVALID),            # slices are chunk aligned
     (dict(path_hi=2**20 + 1), _lib.HMC_E_INVALID),
     (dict(n_steps_avg=251), _lib.HMC_E_INVALID),      # european fixes at n_steps
