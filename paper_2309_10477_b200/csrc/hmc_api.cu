@@ -607,7 +607,8 @@ int hmc_surface_partials(const hmc_model* model, const hmc_surface_spec* spec, c
     int dev = 0, sms = 148;
     HMC_CK(cudaGetDevice(&dev));
     HMC_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const int grid_x = (int)(n_tiles < sms ? n_tiles : sms);
+    const long long slots = (long long)sms * hmc::kSurfMinBlocks;
+    const int grid_x = (int)(n_tiles < slots ? n_tiles : slots);
     HMC_CK(hmc::launch_surface(S.P.a, S.s, n_tiles, grid_x, st));
     return HMC_OK;
 }

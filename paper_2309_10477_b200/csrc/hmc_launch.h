@@ -8,7 +8,14 @@
 namespace hmc {
 
 // ---- strike x maturity surface (hmc_surface.cu) ---------------------------
-constexpr int kSurfThreads = 1024;      // paths per tile (one block)
+#ifndef HMC_SURF_THREADS
+#define HMC_SURF_THREADS 1024
+#endif
+#ifndef HMC_SURF_MINB
+#define HMC_SURF_MINB 1
+#endif
+constexpr int kSurfThreads = HMC_SURF_THREADS;  // paths per tile (one block)
+constexpr int kSurfMinBlocks = HMC_SURF_MINB;   // resident blocks per SM
 constexpr int kSurfMaxStrikes = HMC_SURF_MAX_STRIKES;
 constexpr int kSurfMaxMats = HMC_SURF_MAX_MATS;
 // Per (style, maturity): kSurfVals rows of nK + 1 columns.

@@ -146,7 +146,7 @@ __device__ __forceinline__ void surface_checkpoint(const PathState32& st, const 
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(kSurfThreads, 1) surface_kernel(const KernelArgs a, const SurfArgs s,
+__global__ void __launch_bounds__(kSurfThreads, kSurfMinBlocks) surface_kernel(const KernelArgs a, const SurfArgs s,
                                                                   long long n_tiles) {
     extern __shared__ int hist[];  // [2][kSurfVals][nK + 1] int32 fixed point
     __shared__ float sK[kSurfMaxStrikes];

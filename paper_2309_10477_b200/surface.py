@@ -127,17 +127,16 @@ def summarise(job: SurfaceJob, sums: np.ndarray, wall_ms: float) -> SurfaceResul
     M = N * R
     res = SurfaceResult(strikes=job.strikes.copy(), maturities=job.maturities.copy(),
                         wall_ms=wall_ms, n_paths=N, n_runs=R)
+    s1, s2 = sums[..., 0::2], sums[..., 1::2]          # (R, style, mat, strike, quantity)
+    runs = s1 / N
+    est = runs.mean(axis=0)
+    sd = runs.std(axis=0, ddof=1) if R > 1 else np.zeros_like(est)
+    tot, tot2 = s1.sum(axis=0), s2.sum(axis=0)
+    pse = np.sqrt(np.maximum(tot2 - tot * tot / M, 0.0) / max(M - 1, 1) / M)
     for si, style in enumerate(STYLES):
-        res.estimate[style], res.std_error[style], res.path_std_error[style] = {}, {}, {}
-        for q, name in enumerate(_lib.QUANTITIES):
-            s1 = sums[:, si, :, :, 2 * q]
-            s2 = sums[:, si, :, :, 2 * q + 1]
-            runs = s1 / N
-            res.estimate[style][name] = runs.mean(axis=0)
-            res.std_error[style][name] = runs.std(axis=0, ddof=1) if R > 1 else np.zeros_like(runs[0])
-            tot, tot2 = s1.sum(axis=0), s2.sum(axis=0)
-            var = np.maximum(tot2 - tot * tot / M, 0.0) / max(M - 1, 1)
-            res.path_std_error[style][name] = np.sqrt(var / M)
+        res.estimate[style] = {n: est[si, ..., q] for q, n in enumerate(_lib.QUANTITIES)}
+        res.std_error[style] = {n: sd[si, ..., q] for q, n in enumerate(_lib.QUANTITIES)}
+        res.path_std_error[style] = {n: pse[si, ..., q] for q, n in enumerate(_lib.QUANTITIES)}
     return res
 
 
