@@ -72,6 +72,12 @@ def secondary_workloads(reps: int = 3) -> dict:
                                                sobol_highdim_ack=True, sobol_scramble=True,
                                                n_paths=2**22, n_steps=252, n_runs=1, seed=7)),
             2**22 * 252),
+        "c4_sobol_rqmc_bridge16_asian_full_greeks_2^22x252": (
+            lambda: greeks(p, asian, SimConfig(scheme="milstein", sampler="sobol",
+                                               sobol_highdim_ack=True, sobol_scramble=True,
+                                               sobol_bridge=16, n_paths=2**22, n_steps=252,
+                                               n_runs=1, seed=7)),
+            2**22 * 252),
         "exact_bk_european_price_2^17": (
             lambda: greeks(p, euro, SimConfig(scheme="exact", n_paths=2**17, n_steps=1, n_runs=1,
                                               seed=7)), 2**17),

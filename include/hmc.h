@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define HMC_ABI_VERSION 1
+#define HMC_ABI_VERSION 2
 
 /* reduction geometry -- fixed so results never depend on grid size or GPU count */
 #define HMC_TILE 128          /* paths per thread block == per tile partial   */
@@ -45,6 +45,7 @@ extern "C" {
 #define HMC_CHUNK (HMC_TILE * HMC_CHUNK_TILES) /* 16384 paths per chunk      */
 #define HMC_NQ 7              /* per-path quantities, order below             */
 #define HMC_NW (2 * HMC_NQ)   /* {sum, sum of squares} per quantity           */
+#define HMC_BRIDGE_MAX_SEGMENTS 64 /* Sobol Brownian-bridge skeleton size   */
 
 /* quantity index q: partial[2*q] = sum_x, partial[2*q+1] = sum_x^2 */
 enum {
@@ -114,6 +115,13 @@ typedef struct hmc_sim {
                                   current device; 0: host pointer            */
     int32_t sobol_scramble;    /* sobol only: random digital shift per (run,
                                   dimension) from the seed (randomised QMC)  */
+    int32_t sobol_bridge;      /* sobol only: 0 = dimensions in time order (the
+                                  reference, engine.py:97-101); S > 0 = Brownian
+                                  bridge: the first S dimension pairs build a
+                                  skeleton of both Brownian motions at S
+                                  segment ends, the rest fill each segment by
+                                  conditional (bridge) sampling in time order.
+                                  1 <= S <= min(HMC_BRIDGE_MAX_SEGMENTS, steps) */
 } hmc_sim;
 
 int hmc_abi_version(void);

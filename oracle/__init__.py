@@ -174,6 +174,26 @@ def greeks_paths(params, spec, n_steps, milstein, path_lo, path_hi, key_run,
     return out
 
 
+def greeks_paths_z(params, spec, n_steps, milstein, normals, avg_indices, bumps,
+                   want_greeks=True) -> np.ndarray:
+    """``greeks_paths`` driven by given step normals ``(n, 2*n_steps)``
+    ``[z1, z2]`` (z2 already correlated) instead of uniforms -- for samplers
+    that build the normals differently (``oracle.bridge``)."""
+    z = np.ascontiguousarray(normals, dtype=np.float64)
+    n = z.shape[0]
+    out = np.empty((n, 7))
+    avg = np.ascontiguousarray(avg_indices, dtype=np.int64)
+    pr = _Product(int(spec.is_asian), int(spec.right == "call"), spec.strike,
+                  spec.maturity, spec.spot)
+    b = _Bumps(*[float(x) for x in bumps])
+    rc = lib().hmo_greeks_paths_z(
+        ctypes.byref(_params(params)), ctypes.byref(pr), int(n_steps), int(bool(milstein)), n,
+        _pd(z), avg.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), avg.size, ctypes.byref(b),
+        int(bool(want_greeks)), _pd(out))
+    assert rc == 0
+    return out
+
+
 # ---- the reference's own compiled kernel (oracle/_ref) -------------------
 
 _ref_core = None

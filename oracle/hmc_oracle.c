@@ -121,25 +121,35 @@ typedef struct {
     double s_T, avg, tw;
 } hmo_obs;
 
+/* zrow (optional): the step normals themselves, (z1, z2) per step with z2
+ * already correlated -- for samplers that build normals some other way
+ * (oracle/bridge.py: Sobol Brownian-bridge ordering) */
 static hmo_obs simulate_one(const hmo_params* p, double s0, double v0, double r,
                             double T, int n_steps, int milstein, uint64_t main_key,
-                            const double* urow, const unsigned char* is_avg,
-                            int64_t n_dates) {
+                            const double* urow, const double* zrow,
+                            const unsigned char* is_avg, int64_t n_dates) {
     const double kappa = p->kappa, theta = p->theta, sigma = p->sigma, rho = p->rho;
     const double dt = T / n_steps;
     const double sq1mr2 = sqrt(1.0 - rho * rho);
     double s = s0, v = v0, price_sum = 0.0, tw_sum = 0.0;
     for (int k = 1; k <= n_steps; ++k) {
-        double u1, u2;
-        if (urow) {
+        double u1 = 0.0, u2 = 0.0;
+        if (zrow) {
+        } else if (urow) {
             u1 = urow[2 * (k - 1)];
             u2 = urow[2 * (k - 1) + 1];
         } else {
             u1 = hmo_uniform_at(main_key, (uint64_t)(2 * (k - 1)));
             u2 = hmo_uniform_at(main_key, (uint64_t)(2 * (k - 1) + 1));
         }
-        double z1 = hmo_ndtri(u1);
-        double z2 = rho * z1 + sq1mr2 * hmo_ndtri(u2);
+        double z1, z2;
+        if (zrow) {
+            z1 = zrow[2 * (k - 1)];
+            z2 = zrow[2 * (k - 1) + 1];
+        } else {
+            z1 = hmo_ndtri(u1);
+            z2 = rho * z1 + sq1mr2 * hmo_ndtri(u2);
+        }
         double sqv = sqrt(v * dt);
         s = s * exp((r - 0.5 * v) * dt + sqv * z1);
         double v_new = v + kappa * (theta - v) * dt + sigma * sqv * z2;
@@ -174,7 +184,7 @@ int hmo_discretised_batch(const hmo_params* p, double s0, double T, int n_steps,
         uint64_t main_key = hmo_derive(hmo_derive(key_run, (uint64_t)(path_lo + i)), 0);
         const double* urow = uniforms ? uniforms + (size_t)i * 2 * n_steps : NULL;
         hmo_obs o = simulate_one(p, s0, p->v0, p->r, T, n_steps, milstein, main_key,
-                                 urow, m, n_avg);
+                                 urow, NULL, m, n_avg);
         out[3 * i + 0] = o.s_T;
         out[3 * i + 1] = o.avg;
         out[3 * i + 2] = o.tw;
@@ -214,10 +224,10 @@ static double pw_rho(const hmo_product* pr, hmo_obs o, double disc) {
  * Every bumped value is a full re-simulation with the same uniforms (common
  * random numbers), exactly as the reference's FD tests do.  With
  * want_greeks == 0 only column 0 is filled (the rest are 0). */
-int hmo_greeks_paths(const hmo_params* p, const hmo_product* pr, int n_steps, int milstein,
-                     int64_t path_lo, int64_t path_hi, uint64_t key_run,
-                     const double* uniforms, const int64_t* avg_idx, int64_t n_avg,
-                     const hmo_bumps* b, int want_greeks, double* out) {
+static int greeks_impl(const hmo_params* p, const hmo_product* pr, int n_steps, int milstein,
+                       int64_t path_lo, int64_t path_hi, uint64_t key_run,
+                       const double* uniforms, const double* normals, const int64_t* avg_idx,
+                       int64_t n_avg, const hmo_bumps* b, int want_greeks, double* out) {
     unsigned char* m = avg_mask(n_steps, avg_idx, n_avg);
     if (!m) return 1;
     const double T = pr->maturity, S0 = pr->spot, r = p->r;
@@ -225,31 +235,48 @@ int hmo_greeks_paths(const hmo_params* p, const hmo_product* pr, int n_steps, in
     for (int64_t i = 0; i < path_hi - path_lo; ++i) {
         uint64_t key = hmo_derive(hmo_derive(key_run, (uint64_t)(path_lo + i)), 0);
         const double* urow = uniforms ? uniforms + (size_t)i * 2 * n_steps : NULL;
+        const double* zrow = normals ? normals + (size_t)i * 2 * n_steps : NULL;
         double* o = out + 7 * i;
         memset(o, 0, 7 * sizeof(double));
-        hmo_obs base = simulate_one(p, S0, p->v0, r, T, n_steps, milstein, key, urow, m, n_avg);
+        hmo_obs base = simulate_one(p, S0, p->v0, r, T, n_steps, milstein, key, urow, zrow, m, n_avg);
         o[0] = disc_payoff(pr, underlying(pr, base), disc);
         if (!want_greeks) continue;
         o[1] = pw_delta(pr, base, disc, S0);
         o[2] = pw_rho(pr, base, disc);
         const double h = b->h_spot;
-        hmo_obs su = simulate_one(p, S0 + h, p->v0, r, T, n_steps, milstein, key, urow, m, n_avg);
-        hmo_obs sd = simulate_one(p, S0 - h, p->v0, r, T, n_steps, milstein, key, urow, m, n_avg);
+        hmo_obs su = simulate_one(p, S0 + h, p->v0, r, T, n_steps, milstein, key, urow, zrow, m, n_avg);
+        hmo_obs sd = simulate_one(p, S0 - h, p->v0, r, T, n_steps, milstein, key, urow, zrow, m, n_avg);
         o[3] = (pw_delta(pr, su, disc, S0 + h) - pw_delta(pr, sd, disc, S0 - h)) / (2.0 * h);
         o[5] = (disc_payoff(pr, underlying(pr, su), disc) -
                 disc_payoff(pr, underlying(pr, sd), disc)) / (2.0 * h);
-        hmo_obs vu = simulate_one(p, S0, b->v0_up, r, T, n_steps, milstein, key, urow, m, n_avg);
-        hmo_obs vd = simulate_one(p, S0, b->v0_dn, r, T, n_steps, milstein, key, urow, m, n_avg);
+        hmo_obs vu = simulate_one(p, S0, b->v0_up, r, T, n_steps, milstein, key, urow, zrow, m, n_avg);
+        hmo_obs vd = simulate_one(p, S0, b->v0_dn, r, T, n_steps, milstein, key, urow, zrow, m, n_avg);
         o[4] = (disc_payoff(pr, underlying(pr, vu), disc) -
                 disc_payoff(pr, underlying(pr, vd), disc)) / (b->v0_up - b->v0_dn);
         const double hr = b->h_r;
-        hmo_obs ru = simulate_one(p, S0, p->v0, r + hr, T, n_steps, milstein, key, urow, m, n_avg);
-        hmo_obs rd = simulate_one(p, S0, p->v0, r - hr, T, n_steps, milstein, key, urow, m, n_avg);
+        hmo_obs ru = simulate_one(p, S0, p->v0, r + hr, T, n_steps, milstein, key, urow, zrow, m, n_avg);
+        hmo_obs rd = simulate_one(p, S0, p->v0, r - hr, T, n_steps, milstein, key, urow, zrow, m, n_avg);
         o[6] = (disc_payoff(pr, underlying(pr, ru), exp(-(r + hr) * T)) -
                 disc_payoff(pr, underlying(pr, rd), exp(-(r - hr) * T))) / (2.0 * hr);
     }
     free(m);
     return 0;
+}
+
+int hmo_greeks_paths(const hmo_params* p, const hmo_product* pr, int n_steps, int milstein,
+                     int64_t path_lo, int64_t path_hi, uint64_t key_run,
+                     const double* uniforms, const int64_t* avg_idx, int64_t n_avg,
+                     const hmo_bumps* b, int want_greeks, double* out) {
+    return greeks_impl(p, pr, n_steps, milstein, path_lo, path_hi, key_run, uniforms, NULL,
+                       avg_idx, n_avg, b, want_greeks, out);
+}
+
+/* same, driven by given step normals (n, 2*n_steps) row-major [z1, z2] */
+int hmo_greeks_paths_z(const hmo_params* p, const hmo_product* pr, int n_steps, int milstein,
+                       int64_t n, const double* normals, const int64_t* avg_idx, int64_t n_avg,
+                       const hmo_bumps* b, int want_greeks, double* out) {
+    return greeks_impl(p, pr, n_steps, milstein, 0, n, 0, NULL, normals, avg_idx, n_avg, b,
+                       want_greeks, out);
 }
 
 int hmo_abi_version(void) { return 1; }

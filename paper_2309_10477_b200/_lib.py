@@ -20,7 +20,7 @@ LIB_PATH = os.environ.get("HMC_LIB_PATH") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "libhmc.so")
 
 # mirrors of include/hmc.h
-HMC_ABI_VERSION = 1
+HMC_ABI_VERSION = 2
 HMC_TILE = 128
 HMC_CHUNK_TILES = 128
 HMC_CHUNK = HMC_TILE * HMC_CHUNK_TILES
@@ -47,6 +47,7 @@ EXPORTS = (
 )
 HMC_SURF_MAX_STRIKES = 128
 HMC_SURF_MAX_MATS = 32
+HMC_BRIDGE_MAX_SEGMENTS = 64
 HMC_SURF_VALS = 23
 
 
@@ -70,7 +71,8 @@ class Sim(ctypes.Structure):
                 ("h_spot", ctypes.c_double), ("v0_up", ctypes.c_double),
                 ("v0_dn", ctypes.c_double), ("h_r", ctypes.c_double),
                 ("sobol_v", ctypes.POINTER(ctypes.c_uint32)),
-                ("sobol_v_on_device", ctypes.c_int32), ("sobol_scramble", ctypes.c_int32)]
+                ("sobol_v_on_device", ctypes.c_int32), ("sobol_scramble", ctypes.c_int32),
+                ("sobol_bridge", ctypes.c_int32)]
 
 
 class SurfaceSpec(ctypes.Structure):

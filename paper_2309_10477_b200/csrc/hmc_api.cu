@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "hmc_device.cuh"
@@ -48,9 +49,56 @@ struct Prepared {
     KernelArgs a{};
     std::vector<StepD> st64;
     std::vector<float4> st32;
+    std::vector<hmc::BridgeNodeD> bn64;
+    std::vector<hmc::BridgeStepD> bs64;
+    std::vector<hmc::BridgeNode> bn32;
+    std::vector<hmc::BridgeStep> bs32;
     long long n_tiles = 0, n_chunks = 0;
-    size_t off_st64 = 0, off_st32 = 0, off_sobol = 0, bytes = 0;
+    size_t off_st64 = 0, off_st32 = 0, off_sobol = 0, off_bridge = 0, bytes = 0;
 };
+
+// workspace bytes of the bridge tables (S nodes, n_steps + 1 steps, both precisions)
+size_t bridge_bytes(int S, int n_steps) {
+    if (S <= 0) return 0;
+    const size_t n = (size_t)n_steps + 1;
+    return align_up(S * sizeof(hmc::BridgeNodeD)) + align_up(n * sizeof(hmc::BridgeStepD)) +
+           align_up(S * sizeof(hmc::BridgeNode)) + align_up(n * sizeof(hmc::BridgeStep));
+}
+
+// Brownian-bridge tables over steps 1..n_sim with S segments (layout and
+// formulas: hmc_device.cuh BridgeNodeD).  Level order: the root (W at the
+// horizon) first, then the midpoint of every interval of the previous level,
+// left to right -- the coarsest scales get the lowest Sobol dimensions.
+void build_bridge(int S, int n_sim, double dt, Prepared& P) {
+    std::vector<long long> b((size_t)S + 1);
+    for (int j = 0; j <= S; ++j) b[j] = (long long)j * n_sim / S;
+    auto t = [&](int j) { return (double)b[j] * dt; };
+    P.bn64.clear();
+    P.bn64.push_back({0.0, std::sqrt(t(S)), S, 0, 0, 0});
+    std::vector<std::pair<int, int>> level{{0, S}};
+    while (!level.empty()) {
+        std::vector<std::pair<int, int>> next;
+        for (auto [l, r] : level) {
+            if (r - l < 2) continue;
+            const int m = (l + r) / 2;
+            const double tl = t(l), tm = t(m), tr = t(r);
+            P.bn64.push_back({(tm - tl) / (tr - tl), std::sqrt((tm - tl) * (tr - tm) / (tr - tl)), m, l, r, 0});
+            next.push_back({l, m});
+            next.push_back({m, r});
+        }
+        level.swap(next);
+    }
+    P.bs64.assign((size_t)n_sim + 1, hmc::BridgeStepD{0.0, 0.0, 0, 0});
+    for (int j = 1; j <= S; ++j)
+        for (long long k = b[j - 1] + 1; k <= b[j]; ++k) {
+            const double left = (double)(b[j] - k);  // steps after k inside the segment
+            P.bs64[k] = {1.0 / (left + 1.0), std::sqrt(dt * left / (left + 1.0)), j, k < b[j] ? 1 : 0};
+        }
+    P.bn32.clear();
+    for (const auto& n : P.bn64) P.bn32.push_back({(float)n.a, (float)n.sd, n.m, n.l | (n.r << 16)});
+    P.bs32.clear();
+    for (const auto& st : P.bs64) P.bs32.push_back({(float)st.alpha, (float)st.beta, st.j, st.consume});
+}
 
 int check_model(const hmc_model* m) {
     if (!m) return fail(HMC_E_INVALID, "model is NULL");
@@ -155,6 +203,13 @@ int prepare(const hmc_model* m, const hmc_product* pr, const hmc_sim* sim, Prepa
         if (1.0 + blocks * (double)sim->n_paths > 1073741824.0)
             return fail(HMC_E_INVALID, "sobol index range exceeds 2^30 points");
     }
+    if (sim->sobol_bridge != 0) {
+        if (sim->sampler != HMC_SAMPLER_SOBOL)
+            return fail(HMC_E_INVALID, "the Brownian bridge orders Sobol dimensions (sampler must be sobol)");
+        if (sim->sobol_bridge < 0 || sim->sobol_bridge > HMC_BRIDGE_MAX_SEGMENTS ||
+            sim->sobol_bridge > pr->avg_idx[pr->n_avg - 1])
+            return fail(HMC_E_INVALID, "sobol_bridge must lie in [1, min(HMC_BRIDGE_MAX_SEGMENTS, simulated steps)]");
+    }
 
     KernelArgs& a = P.a;
     a.kappa = m->kappa; a.theta = m->theta; a.sigma = m->sigma; a.rho = m->rho;
@@ -191,6 +246,8 @@ int prepare(const hmc_model* m, const hmc_product* pr, const hmc_sim* sim, Prepa
     std::vector<unsigned char> fix((size_t)sim->n_steps + 1, 0);
     for (long long i = 0; i < pr->n_avg; ++i) fix[pr->avg_idx[i]] = 1;
     build_steps(sim->n_steps, pr->maturity, a.h_r, pr->spot, m->r, fix.data(), P);
+    a.bridge_segments = sim->sobol_bridge;
+    if (a.bridge_segments > 0) build_bridge(a.bridge_segments, a.n_sim, a.dt, P);
 
     const long long n = sim->path_hi - sim->path_lo;
     P.n_tiles = n_tiles_of(n);
@@ -203,6 +260,8 @@ int prepare(const hmc_model* m, const hmc_product* pr, const hmc_sim* sim, Prepa
     P.off_sobol = off;
     if (sim->sampler == HMC_SAMPLER_SOBOL && !sim->sobol_v_on_device)
         off += align_up((size_t)30 * a.sobol_dim * sizeof(uint32_t));
+    P.off_bridge = off;
+    off += bridge_bytes(a.bridge_segments, sim->n_steps);
     P.bytes = off;
     return HMC_OK;
 }
@@ -413,6 +472,8 @@ int64_t hmc_workspace_bytes(const hmc_sim* sim) {
     b += align_up(((size_t)sim->n_steps + 1) * sizeof(float4));
     if (sim->sampler == HMC_SAMPLER_SOBOL && !sim->sobol_v_on_device)
         b += align_up((size_t)30 * 2 * sim->n_steps * sizeof(uint32_t));
+    if (sim->sobol_bridge > 0 && sim->sobol_bridge <= HMC_BRIDGE_MAX_SEGMENTS)
+        b += bridge_bytes(sim->sobol_bridge, sim->n_steps);
     return (int64_t)b;
 }
 
@@ -440,6 +501,26 @@ int hmc_greeks_chunks(const hmc_model* model, const hmc_product* product, const 
                                    cudaMemcpyHostToDevice, s));
             P.a.sobol_v = (const uint32_t*)(w + P.off_sobol);
         }
+    }
+    if (P.a.bridge_segments > 0) {
+        char* b = w + P.off_bridge;
+        const size_t sz[4] = {P.bn64.size() * sizeof(hmc::BridgeNodeD), P.bs64.size() * sizeof(hmc::BridgeStepD),
+                              P.bn32.size() * sizeof(hmc::BridgeNode), P.bs32.size() * sizeof(hmc::BridgeStep)};
+        const void* src[4] = {P.bn64.data(), P.bs64.data(), P.bn32.data(), P.bs32.data()};
+        // region strides as bridge_bytes(): S node slots, n_steps + 1 step slots
+        const size_t S = (size_t)P.a.bridge_segments, n1 = (size_t)sim->n_steps + 1;
+        const size_t stride[4] = {align_up(S * sizeof(hmc::BridgeNodeD)), align_up(n1 * sizeof(hmc::BridgeStepD)),
+                                  align_up(S * sizeof(hmc::BridgeNode)), align_up(n1 * sizeof(hmc::BridgeStep))};
+        char* dst[4];
+        for (int i = 0; i < 4; ++i) {
+            dst[i] = b;
+            HMC_CK(cudaMemcpyAsync(b, src[i], sz[i], cudaMemcpyHostToDevice, s));
+            b += stride[i];
+        }
+        P.a.bridge_nodes64 = (const hmc::BridgeNodeD*)dst[0];
+        P.a.bridge_steps64 = (const hmc::BridgeStepD*)dst[1];
+        P.a.bridge_nodes32 = (const hmc::BridgeNode*)dst[2];
+        P.a.bridge_steps32 = (const hmc::BridgeStep*)dst[3];
     }
     if (sim->precision == HMC_PREC_FP64)
         HMC_CK(hmc::launch_replay_greeks(P.a, d_tiles, P.n_tiles, s));

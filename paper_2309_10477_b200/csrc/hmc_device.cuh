@@ -33,6 +33,32 @@ struct StepD {
     double t, e1p, e1m, fix;
 };
 
+// Sobol Brownian bridge (hmc_sim.sobol_bridge = S > 0).  Skeleton points
+// j = 0..S sit at steps b_j = floor(j n_sim / S) (point 0 = origin, W = 0);
+// node i (level order, dimension pair i) sets
+//   W(b_m) = W(b_l) + a (W(b_r) - W(b_l)) + sd z      (root: l = r = 0)
+// and step k of segment j (b_{j-1} < k <= b_j) draws its increment as
+//   dW_k = (W(b_j) - W_{k-1}) alpha_k + beta_k z
+// with alpha_k = 1 / (b_j - k + 1), beta_k = sqrt(dt (b_j - k) / (b_j - k + 1));
+// segment ends (k = b_j) have alpha = 1, beta = 0 and consume no pair; the
+// other steps take the next pair S, S+1, ... in time order.
+struct BridgeNodeD {
+    double a, sd;
+    int m, l, r, pad;
+};
+struct BridgeStepD {
+    double alpha, beta;
+    int j, consume;
+};
+struct BridgeNode {
+    float a, sd;
+    int m, lr;  // l | r << 16
+};
+struct BridgeStep {
+    float alpha, beta;
+    int j, consume;
+};
+
 struct KernelArgs {
     // model (HestonParams) and product (OptionSpec)
     double kappa, theta, sigma, rho, r, v0;
@@ -57,6 +83,11 @@ struct KernelArgs {
     const uint32_t* sobol_v;    // [30][sobol_dim]
     int sobol_dim;
     int sobol_scramble;         // random digital shift per (run, dimension)
+    int bridge_segments;        // S: Sobol Brownian bridge (0 = time order)
+    const BridgeNodeD* bridge_nodes64;  // [S]
+    const BridgeStepD* bridge_steps64;  // [n_sim + 1]
+    const BridgeNode* bridge_nodes32;   // [S]
+    const BridgeStep* bridge_steps32;   // [n_sim + 1]
     // fp32 derived constants (host-computed in fp64, rounded once)
     float f_omkdt;   // 1 - kappa dt
     float f_ck0;     // kappa theta dt - milstein * sigma^2 dt / 4

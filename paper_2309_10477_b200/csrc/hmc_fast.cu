@@ -35,10 +35,12 @@
 // daily-fixing Asian is MUFU-queue bound and prefers 7 blocks (28 warps,
 // 72 regs: 48 warps 11.1 ms -> 28 warps 10.7 ms); the European (one ex2 at
 // the end) prefers 10 blocks (8.55 -> 8.40 ms).
+// The Brownian-bridge Sobol kernel keeps its skeleton in shared memory
+// (20 KB tables + (S + 1) KB skeleton per block), 6 blocks at S = 16.
 #ifdef HMC_MIN_BLOCKS
 #define HMC_BOUNDS __launch_bounds__(kTile, HMC_MIN_BLOCKS)
 #else
-#define HMC_BOUNDS __launch_bounds__(kTile, (FIX == kFixLast ? 10 : 7))
+#define HMC_BOUNDS __launch_bounds__(kTile, (SAMPLER == kSamplerBridge ? 6 : (FIX == kFixLast ? 10 : 7)))
 #endif
 
 namespace hmc {
@@ -61,67 +63,149 @@ struct SobolTables {
     uint2 U[kWarps][2][kSobolSteps];   // per warp: blocks B1, B2
 };
 
+constexpr int kSamplerBridge = 2;  // internal: Sobol with Brownian-bridge ordering
+static_assert(HMC_BRIDGE_MAX_SEGMENTS <= kSobolSteps, "skeleton pairs must sit in the first table chunk");
+
+// Gray-code split of this thread's point index (see above)
+struct SobolLane {
+    uint32_t gB1, gB2;  // Gray codes of the warp's two aligned 32-point blocks
+    int which;          // this lane's block
+    uint32_t jl;        // Gray code of the lane part
+    unsigned long long key_run;
+    float half;         // 0.5: cell midpoints of shifted points
+
+    __device__ __forceinline__ SobolLane(int run, long long p, const KernelArgs& a) {
+        // scrambled (randomised QMC): every run re-uses points 1..N under its own shifts
+        const uint32_t n = (uint32_t)(1 + (a.sobol_scramble ? 0LL : (long long)run * a.n_paths) + p);
+        const uint32_t n0 = __shfl_sync(0xffffffffu, n, 0);
+        const uint32_t B1 = n0 & ~31u;
+        gB1 = B1 ^ (B1 >> 1);
+        gB2 = (B1 + 32) ^ ((B1 + 32) >> 1);
+        which = ((n & ~31u) != B1) ? 1 : 0;
+        const uint32_t c = n & 31u;
+        jl = c ^ (c >> 1);
+        key_run = derive(a.root_key, (unsigned long long)run);
+        half = a.sobol_scramble ? 0.5f : 0.0f;
+    }
+};
+
+// (re)build the tables for dimension pairs [q0, q0 + m); block-wide
+__device__ __forceinline__ void sobol_refill(SobolTables& tab, int q0, int m, const SobolLane& sl,
+                                             const KernelArgs& a) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t* __restrict__ V = a.sobol_v;
+    const int dim = a.sobol_dim;
+    const int d0 = 2 * q0;
+    __syncthreads();  // previous chunk fully consumed
+    // lane-part table: thread t owns dimension d0 + t, all 32 Gray codes
+    if (threadIdx.x < 2 * m) {
+        const int d = d0 + threadIdx.x;
+        uint32_t v[5];
+#pragma unroll
+        for (int b = 0; b < 5; ++b) v[b] = __ldg(V + b * dim + d);
+        uint32_t x[32];
+        x[0] = 0;
+#pragma unroll
+        for (int j = 1; j < 32; ++j) x[j] = x[j & (j - 1)] ^ v[__ffs(j) - 1];
+        uint32_t* col = reinterpret_cast<uint32_t*>(&tab.T[threadIdx.x >> 1][0]) + (threadIdx.x & 1);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) col[2 * j] = x[j];
+    }
+    // warp-uniform parts for this warp's two aligned blocks
+    for (int dd = lane; dd < 2 * m; dd += 32) {
+        const int d = d0 + dd;
+        uint32_t u1 = 0, u2d = 0;
+        for (int b = 4; b < kSobolBits; ++b) {
+            const uint32_t vb = ((sl.gB1 | (sl.gB1 ^ sl.gB2)) >> b) & 1u ? __ldg(V + b * dim + d) : 0u;
+            if ((sl.gB1 >> b) & 1u) u1 ^= vb;
+            if (((sl.gB1 ^ sl.gB2) >> b) & 1u) u2d ^= vb;
+        }
+        if (a.sobol_scramble) u1 ^= sobol_shift(sl.key_run, d);
+        reinterpret_cast<uint32_t*>(&tab.U[warp][0][dd >> 1])[dd & 1] = u1;
+        reinterpret_cast<uint32_t*>(&tab.U[warp][1][dd >> 1])[dd & 1] = u1 ^ u2d;
+    }
+    __syncthreads();
+}
+
+// the two standard normals of pair q of the loaded chunk
+__device__ __forceinline__ void sobol_pair(const SobolTables& tab, int q, const SobolLane& sl,
+                                           float& za, float& zb) {
+    const uint2 t = tab.T[q][sl.jl];
+    const uint2 u = tab.U[threadIdx.x >> 5][sl.which][q];
+    za = sobol_normal(t.x ^ u.x, sl.half);
+    zb = sobol_normal(t.y ^ u.y, sl.half);
+}
+
 template <int FIX, bool GREEKS>
 __device__ __forceinline__ void sobol_paths(PathState32& st, int run, long long p, const KernelArgs& a) {
     __shared__ SobolTables tab;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // scrambled (randomised QMC): every run re-uses points 1..N under its own shifts
-        const uint32_t n = (uint32_t)(1 + (a.sobol_scramble ? 0LL : (long long)run * a.n_paths) + p);
-    const uint32_t n0 = __shfl_sync(0xffffffffu, n, 0);
-    const uint32_t B1 = n0 & ~31u;
-    const uint32_t gB1 = B1 ^ (B1 >> 1), gB2 = (B1 + 32) ^ ((B1 + 32) >> 1);
-    const int which = ((n & ~31u) != B1) ? 1 : 0;
-    const uint32_t c = n & 31u, jl = c ^ (c >> 1);
-    const unsigned long long key_run = derive(a.root_key, (unsigned long long)run);
-    const uint32_t* __restrict__ V = a.sobol_v;
-    const int dim = a.sobol_dim;
+    const SobolLane sl(run, p, a);
     const float c1 = a.f_sqdt * a.f_log2e;
     const float cs = a.f_sigma * a.f_sqdt;
-    const float half = a.sobol_scramble ? 0.5f : 0.0f;
 
 #pragma unroll 1
     for (int k0 = 1; k0 <= a.n_sim; k0 += kSobolSteps) {
         const int m = min(kSobolSteps, a.n_sim - k0 + 1);
-        const int d0 = 2 * (k0 - 1);
-        __syncthreads();  // previous chunk fully consumed
-        // lane-part table: thread t owns dimension d0 + t, all 32 Gray codes
-        if (threadIdx.x < 2 * m) {
-            const int d = d0 + threadIdx.x;
-            uint32_t v[5];
-#pragma unroll
-            for (int b = 0; b < 5; ++b) v[b] = __ldg(V + b * dim + d);
-            uint32_t x[32];
-            x[0] = 0;
-#pragma unroll
-            for (int j = 1; j < 32; ++j) x[j] = x[j & (j - 1)] ^ v[__ffs(j) - 1];
-            uint32_t* col = reinterpret_cast<uint32_t*>(&tab.T[threadIdx.x >> 1][0]) + (threadIdx.x & 1);
-#pragma unroll
-            for (int j = 0; j < 32; ++j) col[2 * j] = x[j];
-        }
-        // warp-uniform parts for this warp's two aligned blocks
-        for (int dd = lane; dd < 2 * m; dd += 32) {
-            const int d = d0 + dd;
-            uint32_t u1 = 0, u2d = 0;
-            for (int b = 4; b < kSobolBits; ++b) {
-                const uint32_t vb = ((gB1 | (gB1 ^ gB2)) >> b) & 1u ? __ldg(V + b * dim + d) : 0u;
-                if ((gB1 >> b) & 1u) u1 ^= vb;
-                if (((gB1 ^ gB2) >> b) & 1u) u2d ^= vb;
-            }
-            if (a.sobol_scramble) u1 ^= sobol_shift(key_run, d);
-            reinterpret_cast<uint32_t*>(&tab.U[warp][0][dd >> 1])[dd & 1] = u1;
-            reinterpret_cast<uint32_t*>(&tab.U[warp][1][dd >> 1])[dd & 1] = u1 ^ u2d;
-        }
-        __syncthreads();
+        sobol_refill(tab, k0 - 1, m, sl, a);
 #pragma unroll 1
         for (int q = 0; q < m; ++q) {
-            const uint2 t = tab.T[q][jl];
-            const uint2 u = tab.U[warp][which][q];
-            const float za = sobol_normal(t.x ^ u.x, half);
-            const float zb = sobol_normal(t.y ^ u.y, half);
+            float za, zb;
+            sobol_pair(tab, q, sl, za, zb);
             const float z1l = c1 * za;
             const float sz2 = cs * fmaf(a.f_rho, za, a.f_sq1mr2 * zb);
             step<FIX, GREEKS>(st, k0 + q, z1l, sz2, a);
         }
+    }
+}
+
+// Sobol with Brownian-bridge ordering (hmc_sim.sobol_bridge, tables:
+// hmc_device.cuh BridgeNode): pairs 0..S-1 build this path's skeleton of
+// both Brownian motions in shared memory (dynamic, [S + 1][kTile] float2,
+// conflict-free), then the steps run in time order, each increment drawn
+// conditionally on the segment's right end.  Same dimensions, same table
+// refills as the time-ordered driver; the increments replace sqrt(dt) z.
+template <int FIX, bool GREEKS>
+__device__ __forceinline__ void sobol_bridge_paths(PathState32& st, int run, long long p,
+                                                   const KernelArgs& a) {
+    __shared__ SobolTables tab;
+    extern __shared__ float2 skel[];
+    float2* my = skel + threadIdx.x;  // point j at my[j * kTile]
+    const SobolLane sl(run, p, a);
+    const int S = a.bridge_segments;
+    const float l2e = a.f_log2e, sg = a.f_sigma;
+
+    int c0 = 0;  // first pair of the loaded chunk
+    sobol_refill(tab, 0, min(kSobolSteps, a.n_sim), sl, a);
+    my[0] = make_float2(0.0f, 0.0f);
+#pragma unroll 1
+    for (int i = 0; i < S; ++i) {  // S <= HMC_BRIDGE_MAX_SEGMENTS == kSobolSteps: chunk 0
+        float za, zb;
+        sobol_pair(tab, i, sl, za, zb);
+        const BridgeNode nd = a.bridge_nodes32[i];
+        const float2 wl = my[(nd.lr & 0xffff) * kTile], wr = my[(nd.lr >> 16) * kTile];
+        my[nd.m * kTile] = make_float2(fmaf(nd.sd, za, fmaf(nd.a, wr.x - wl.x, wl.x)),
+                                       fmaf(nd.sd, zb, fmaf(nd.a, wr.y - wl.y, wl.y)));
+    }
+    int pc = S;  // next pair
+    float W1 = 0.0f, W2 = 0.0f;
+#pragma unroll 1
+    for (int k = 1; k <= a.n_sim; ++k) {
+        const BridgeStep bs = a.bridge_steps32[k];
+        float za = 0.0f, zb = 0.0f;
+        if (bs.consume) {
+            if (pc == c0 + kSobolSteps) {
+                c0 = pc;
+                sobol_refill(tab, c0, min(kSobolSteps, a.n_sim - c0), sl, a);
+            }
+            sobol_pair(tab, pc - c0, sl, za, zb);
+            ++pc;
+        }
+        const float2 R = my[bs.j * kTile];
+        const float d1 = fmaf(R.x - W1, bs.alpha, bs.beta * za);
+        const float d2 = fmaf(R.y - W2, bs.alpha, bs.beta * zb);
+        W1 = bs.consume ? W1 + d1 : R.x;
+        W2 = bs.consume ? W2 + d2 : R.y;
+        step<FIX, GREEKS>(st, k, l2e * d1, sg * fmaf(a.f_rho, d1, a.f_sq1mr2 * d2), a);
     }
 }
 
@@ -206,8 +290,10 @@ __global__ void HMC_BOUNDS fast_greeks_kernel(const KernelArgs a,
             step<FIX, GREEKS>(st, k, z1l, sz2, a);
         }
 #endif
-    } else {
+    } else if (SAMPLER == HMC_SAMPLER_SOBOL) {
         sobol_paths<FIX, GREEKS>(st, run, p, a);
+    } else {
+        sobol_bridge_paths<FIX, GREEKS>(st, run, p, a);
     }
     if (FIX == kFixLast) fixing<GREEKS>(st, __ldg(a.steps32 + a.n_sim));
 
@@ -235,8 +321,14 @@ static void launch_sampler(const KernelArgs& a, double* d_tiles, long long n_til
                            cudaStream_t s) {
     if (a.sampler == HMC_SAMPLER_PSEUDO)
         fast_greeks_kernel<FIX, GREEKS, HMC_SAMPLER_PSEUDO><<<grid, kTile, 0, s>>>(a, d_tiles, n_tiles);
-    else
+    else if (a.bridge_segments == 0)
         fast_greeks_kernel<FIX, GREEKS, HMC_SAMPLER_SOBOL><<<grid, kTile, 0, s>>>(a, d_tiles, n_tiles);
+    else {
+        const int smem = (a.bridge_segments + 1) * kTile * (int)sizeof(float2);
+        auto k = fast_greeks_kernel<FIX, GREEKS, kSamplerBridge>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);  // launch reports failure
+        k<<<grid, kTile, smem, s>>>(a, d_tiles, n_tiles);
+    }
 }
 
 template <int FIX>

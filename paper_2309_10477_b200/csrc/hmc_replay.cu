@@ -158,11 +158,7 @@ __global__ void __launch_bounds__(kTile) replay_greeks_kernel(const KernelArgs a
     TrajD tu{a.s0, a.v0_up, 0.0, 0.0};
     TrajD td{a.s0, a.v0_dn, 0.0, 0.0};
     double dp = 0.0, dm = 0.0;
-    for (int k = 1; k <= a.n_sim; ++k) {
-        double u1, u2;
-        dr.get(k, u1, u2);
-        const double z1 = ndtri_ref(u1);
-        const double z2 = a.rho * z1 + a.sq1mr2 * ndtri_ref(u2);
+    auto advance = [&](int k, double z1, double z2) {
         ref_step(t0, z1, z2, a);
         if (GREEKS) {
             ref_step(tu, z1, z2, a);
@@ -178,6 +174,46 @@ __global__ void __launch_bounds__(kTile) replay_greeks_kernel(const KernelArgs a
                 dp += t0.s * st.e1p;
                 dm += t0.s * st.e1m;
             }
+        }
+    };
+    if (a.bridge_segments == 0) {
+        for (int k = 1; k <= a.n_sim; ++k) {
+            double u1, u2;
+            dr.get(k, u1, u2);
+            const double z1 = ndtri_ref(u1);
+            const double z2 = a.rho * z1 + a.sq1mr2 * ndtri_ref(u2);
+            advance(k, z1, z2);
+        }
+    } else {
+        // Sobol Brownian bridge (tables and formulas: hmc_device.cuh
+        // BridgeNodeD); fp64 twin of hmc_fast.cu sobol_bridge_paths
+        double W1s[HMC_BRIDGE_MAX_SEGMENTS + 1], W2s[HMC_BRIDGE_MAX_SEGMENTS + 1];
+        W1s[0] = W2s[0] = 0.0;
+        for (int i = 0; i < a.bridge_segments; ++i) {
+            double u1, u2;
+            dr.get(i + 1, u1, u2);  // dimension pair i
+            const BridgeNodeD nd = a.bridge_nodes64[i];
+            W1s[nd.m] = W1s[nd.l] + nd.a * (W1s[nd.r] - W1s[nd.l]) + nd.sd * ndtri_ref(u1);
+            W2s[nd.m] = W2s[nd.l] + nd.a * (W2s[nd.r] - W2s[nd.l]) + nd.sd * ndtri_ref(u2);
+        }
+        int pc = a.bridge_segments;
+        double W1 = 0.0, W2 = 0.0;
+        const double isq = 1.0 / sqrt(a.dt);
+        for (int k = 1; k <= a.n_sim; ++k) {
+            const BridgeStepD bs = a.bridge_steps64[k];
+            double za = 0.0, zb = 0.0;
+            if (bs.consume) {
+                double u1, u2;
+                dr.get(++pc, u1, u2);  // pair pc - 1
+                za = ndtri_ref(u1);
+                zb = ndtri_ref(u2);
+            }
+            const double d1 = (W1s[bs.j] - W1) * bs.alpha + bs.beta * za;
+            const double d2 = (W2s[bs.j] - W2) * bs.alpha + bs.beta * zb;
+            W1 = bs.consume ? W1 + d1 : W1s[bs.j];
+            W2 = bs.consume ? W2 + d2 : W2s[bs.j];
+            const double z1 = d1 * isq;
+            advance(k, z1, a.rho * z1 + a.sq1mr2 * (d2 * isq));
         }
     }
     // european: the one fixing is t_n = T, so ps = s_T and the reference's

@@ -84,7 +84,7 @@ class Job:
             n_steps=config.n_steps, n_runs=config.n_runs, n_paths=config.n_paths,
             path_lo=0, path_hi=config.n_paths, seed=config.seed & (2**64 - 1),
             h_spot=h_spot, v0_up=v_up, v0_dn=v_dn, h_r=h_r,
-            sobol_scramble=int(bool(config.sobol_scramble)))
+            sobol_scramble=int(bool(config.sobol_scramble)), sobol_bridge=config.sobol_bridge)
         self.sobol_host = None
         if config.sampler == "sobol":
             blocks = 1 if config.sobol_scramble else config.n_runs

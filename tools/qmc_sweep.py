@@ -16,13 +16,14 @@ lo, hi = int(os.environ.get("QMC_LO", "20")), int(os.environ.get("QMC_HI", "26")
 out = {"runs": R, "steps": 252, "params": BENCH_PARAMS, "rows": []}
 for name, spec in specs.items():
     for e in range(lo, hi + 1):
-        for sampler in ("pseudo", "sobol"):
+        for sampler, S in (("pseudo", 0), ("sobol", 0), ("sobol", 16)):
             cfg = SimConfig(scheme="milstein", sampler=sampler, sobol_highdim_ack=True, sobol_scramble=True,
-                            n_paths=2 ** e, n_steps=252, n_runs=R, seed=2024)
+                            sobol_bridge=S, n_paths=2 ** e, n_steps=252, n_runs=R, seed=2024)
             torch.cuda.synchronize(); t0 = time.perf_counter()
             g = greeks(p, spec, cfg)
             torch.cuda.synchronize(); dt = time.perf_counter() - t0
-            row = {"product": name, "log2_n": e, "sampler": sampler, "seconds": dt,
+            row = {"product": name, "log2_n": e, "sampler": sampler + ("+bridge16" if S else ""),
+                   "seconds": dt,
                    "path_steps_per_s": R * 2 ** e * 252 / dt}
             for q in ("price", "delta", "gamma", "vega", "rho"):
                 row[q] = [g[q].estimate, g[q].std_error / math.sqrt(R)]
