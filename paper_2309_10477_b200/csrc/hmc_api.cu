@@ -97,7 +97,7 @@ void build_bridge(int S, int n_sim, double dt, Prepared& P) {
     P.bn32.clear();
     for (const auto& n : P.bn64) P.bn32.push_back({(float)n.a, (float)n.sd, n.m, n.l | (n.r << 16)});
     P.bs32.clear();
-    for (const auto& st : P.bs64) P.bs32.push_back({(float)st.alpha, (float)st.beta, st.j, st.consume});
+    for (const auto& st : P.bs64) P.bs32.push_back({(float)st.alpha, (float)st.beta});
 }
 
 int check_model(const hmc_model* m) {
@@ -247,7 +247,12 @@ int prepare(const hmc_model* m, const hmc_product* pr, const hmc_sim* sim, Prepa
     for (long long i = 0; i < pr->n_avg; ++i) fix[pr->avg_idx[i]] = 1;
     build_steps(sim->n_steps, pr->maturity, a.h_r, pr->spot, m->r, fix.data(), P);
     a.bridge_segments = sim->sobol_bridge;
-    if (a.bridge_segments > 0) build_bridge(a.bridge_segments, a.n_sim, a.dt, P);
+    if (a.bridge_segments > 0) {
+        build_bridge(a.bridge_segments, a.n_sim, a.dt, P);
+        for (size_t k = 1; k < P.bs64.size(); ++k)  // fp32 kernel: beta == 0 marks segment ends
+            if (P.bs64[k].consume && P.bs32[k].beta == 0.0f)
+                return fail(HMC_E_INVALID, "time step too small for the fp32 Brownian bridge");
+    }
 
     const long long n = sim->path_hi - sim->path_lo;
     P.n_tiles = n_tiles_of(n);

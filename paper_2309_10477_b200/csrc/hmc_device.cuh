@@ -54,9 +54,8 @@ struct BridgeNode {
     float a, sd;
     int m, lr;  // l | r << 16
 };
-struct BridgeStep {
-    float alpha, beta;
-    int j, consume;
+struct BridgeStep {  // fp32: the segment index and the pair flag are implied
+    float alpha, beta;  // (beta == 0 exactly at segment ends)
 };
 
 struct KernelArgs {

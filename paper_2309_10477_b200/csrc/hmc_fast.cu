@@ -36,11 +36,11 @@
 // 72 regs: 48 warps 11.1 ms -> 28 warps 10.7 ms); the European (one ex2 at
 // the end) prefers 10 blocks (8.55 -> 8.40 ms).
 // The Brownian-bridge Sobol kernel keeps its skeleton in shared memory
-// (20 KB tables + (S + 1) KB skeleton per block), 6 blocks at S = 16.
+// (10 KB tables + (S + 1) KB skeleton per block), 7 blocks at S = 16.
 #ifdef HMC_MIN_BLOCKS
 #define HMC_BOUNDS __launch_bounds__(kTile, HMC_MIN_BLOCKS)
 #else
-#define HMC_BOUNDS __launch_bounds__(kTile, (SAMPLER == kSamplerBridge ? 6 : (FIX == kFixLast ? 10 : 7)))
+#define HMC_BOUNDS __launch_bounds__(kTile, (SAMPLER == kSamplerBridge ? 7 : (FIX == kFixLast ? 10 : 7)))
 #endif
 
 namespace hmc {
@@ -57,14 +57,22 @@ namespace hmc {
 // (a.sobol_shift) per (run, dimension) for randomised QMC.
 // ---------------------------------------------------------------------------
 constexpr int kSobolSteps = 64;  // steps per table refill (128 dimensions)
+// the bridge driver also holds the skeleton in shared memory: half-size
+// tables keep it at 7 blocks per SM
+#ifndef HMC_BRIDGE_TABLE_STEPS
+#define HMC_BRIDGE_TABLE_STEPS 32
+#endif
+constexpr int kBridgeTableSteps = HMC_BRIDGE_TABLE_STEPS;
 
-struct SobolTables {
-    uint2 T[kSobolSteps][32];          // lane parts, (dim 2q, dim 2q+1)
-    uint2 U[kWarps][2][kSobolSteps];   // per warp: blocks B1, B2
+template <int STEPS>
+struct SobolTablesT {
+    static constexpr int kSteps = STEPS;
+    uint2 T[STEPS][32];          // lane parts, (dim 2q, dim 2q+1)
+    uint2 U[kWarps][2][STEPS];   // per warp: blocks B1, B2
 };
+using SobolTables = SobolTablesT<kSobolSteps>;
 
 constexpr int kSamplerBridge = 2;  // internal: Sobol with Brownian-bridge ordering
-static_assert(HMC_BRIDGE_MAX_SEGMENTS <= kSobolSteps, "skeleton pairs must sit in the first table chunk");
 
 // Gray-code split of this thread's point index (see above)
 struct SobolLane {
@@ -90,7 +98,8 @@ struct SobolLane {
 };
 
 // (re)build the tables for dimension pairs [q0, q0 + m); block-wide
-__device__ __forceinline__ void sobol_refill(SobolTables& tab, int q0, int m, const SobolLane& sl,
+template <class Tab>
+__device__ __forceinline__ void sobol_refill(Tab& tab, int q0, int m, const SobolLane& sl,
                                              const KernelArgs& a) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t* __restrict__ V = a.sobol_v;
@@ -128,7 +137,8 @@ __device__ __forceinline__ void sobol_refill(SobolTables& tab, int q0, int m, co
 }
 
 // the two standard normals of pair q of the loaded chunk
-__device__ __forceinline__ void sobol_pair(const SobolTables& tab, int q, const SobolLane& sl,
+template <class Tab>
+__device__ __forceinline__ void sobol_pair(const Tab& tab, int q, const SobolLane& sl,
                                            float& za, float& zb) {
     const uint2 t = tab.T[q][sl.jl];
     const uint2 u = tab.U[threadIdx.x >> 5][sl.which][q];
@@ -167,7 +177,8 @@ __device__ __forceinline__ void sobol_paths(PathState32& st, int run, long long 
 template <int FIX, bool GREEKS>
 __device__ __forceinline__ void sobol_bridge_paths(PathState32& st, int run, long long p,
                                                    const KernelArgs& a) {
-    __shared__ SobolTables tab;
+    constexpr int kQ = kBridgeTableSteps;
+    __shared__ SobolTablesT<kQ> tab;
     extern __shared__ float2 skel[];
     float2* my = skel + threadIdx.x;  // point j at my[j * kTile]
     const SobolLane sl(run, p, a);
@@ -175,12 +186,16 @@ __device__ __forceinline__ void sobol_bridge_paths(PathState32& st, int run, lon
     const float l2e = a.f_log2e, sg = a.f_sigma;
 
     int c0 = 0;  // first pair of the loaded chunk
-    sobol_refill(tab, 0, min(kSobolSteps, a.n_sim), sl, a);
+    sobol_refill(tab, 0, min(kQ, a.n_sim), sl, a);
     my[0] = make_float2(0.0f, 0.0f);
 #pragma unroll 1
-    for (int i = 0; i < S; ++i) {  // S <= HMC_BRIDGE_MAX_SEGMENTS == kSobolSteps: chunk 0
+    for (int i = 0; i < S; ++i) {
+        if (i == c0 + kQ) {
+            c0 = i;
+            sobol_refill(tab, c0, min(kQ, a.n_sim - c0), sl, a);
+        }
         float za, zb;
-        sobol_pair(tab, i, sl, za, zb);
+        sobol_pair(tab, i - c0, sl, za, zb);
         const BridgeNode nd = a.bridge_nodes32[i];
         const float2 wl = my[(nd.lr & 0xffff) * kTile], wr = my[(nd.lr >> 16) * kTile];
         my[nd.m * kTile] = make_float2(fmaf(nd.sd, za, fmaf(nd.a, wr.x - wl.x, wl.x)),
@@ -188,23 +203,34 @@ __device__ __forceinline__ void sobol_bridge_paths(PathState32& st, int run, lon
     }
     int pc = S;  // next pair
     float W1 = 0.0f, W2 = 0.0f;
+    int j = 1;  // current segment; its right end R stays in registers
+    float2 R = my[kTile];
 #pragma unroll 1
     for (int k = 1; k <= a.n_sim; ++k) {
         const BridgeStep bs = a.bridge_steps32[k];
+        const bool fine = bs.beta != 0.0f;  // segment ends draw nothing
         float za = 0.0f, zb = 0.0f;
-        if (bs.consume) {
-            if (pc == c0 + kSobolSteps) {
+        if (fine) {
+            if (pc == c0 + kQ) {
                 c0 = pc;
-                sobol_refill(tab, c0, min(kSobolSteps, a.n_sim - c0), sl, a);
+                sobol_refill(tab, c0, min(kQ, a.n_sim - c0), sl, a);
             }
             sobol_pair(tab, pc - c0, sl, za, zb);
             ++pc;
         }
-        const float2 R = my[bs.j * kTile];
         const float d1 = fmaf(R.x - W1, bs.alpha, bs.beta * za);
         const float d2 = fmaf(R.y - W2, bs.alpha, bs.beta * zb);
-        W1 = bs.consume ? W1 + d1 : R.x;
-        W2 = bs.consume ? W2 + d2 : R.y;
+        if (fine) {
+            W1 += d1;
+            W2 += d2;
+        } else {
+            W1 = R.x;
+            W2 = R.y;
+            // (a conditional `if (++j <= S) R = my[j * kTile]` here was
+            // miscompiled by ptxas 12.9 into a load one segment too far)
+            j = min(j + 1, S);
+            R = my[j * kTile];
+        }
         step<FIX, GREEKS>(st, k, l2e * d1, sg * fmaf(a.f_rho, d1, a.f_sq1mr2 * d2), a);
     }
 }
