@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <atomic>
 #include <utility>
 #include <vector>
 
@@ -38,6 +39,26 @@ int fail(int code, const std::string& msg) {
 
 using hmc::KernelArgs;
 using hmc::StepD;
+
+// The one-call entry points allocate their device buffers from the
+// device's default stream-ordered pool.  With the pool's default release
+// threshold (0) every synchronize hands the memory back to the driver and
+// the next call maps it again -- 10-20 ms for the exact scheme's 150 MB
+// node cache.  Keep freed blocks in the pool instead (once per device).
+std::atomic<unsigned long long> g_pool_kept{0};
+
+cudaError_t keep_pool_memory(int dev) {
+    if (dev < 0 || dev >= 64) return cudaSuccess;
+    const unsigned long long bit = 1ULL << dev;
+    if (g_pool_kept.load() & bit) return cudaSuccess;
+    cudaMemPool_t pool;
+    cudaError_t e = cudaDeviceGetDefaultMemPool(&pool, dev);
+    if (e != cudaSuccess) return e;
+    uint64_t keep = ~0ULL;
+    e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    if (e == cudaSuccess) g_pool_kept.fetch_or(bit);
+    return e;
+}
 
 constexpr size_t kAlign = 256;
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
@@ -553,6 +574,7 @@ int hmc_greeks(const hmc_model* model, const hmc_product* product, const hmc_sim
     int rc = prepare(model, product, &sim, P);
     if (rc) return rc;
     HMC_CK(cudaSetDevice(device));
+    HMC_CK(keep_pool_memory(device));
     cudaStream_t s;
     HMC_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     const size_t work = (size_t)hmc_workspace_bytes(&sim);
@@ -611,6 +633,7 @@ int hmc_discretised_batch_f64(const hmc_model* model, double s0, double T, int32
     build_steps(n_steps, T, 0.0, s0, model->r, fix.data(), P);
 
     HMC_CK(cudaSetDevice(device));
+    HMC_CK(keep_pool_memory(device));
     cudaStream_t s;
     HMC_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     const size_t ub = uniforms ? (size_t)n * 2 * n_steps * sizeof(double) : 0;
@@ -769,6 +792,7 @@ int hmc_surface(const hmc_model* model, const hmc_surface_spec* spec, const hmc_
     int rc = prepare_surface(model, spec, &sim, S);
     if (rc) return rc;
     HMC_CK(cudaSetDevice(device));
+    HMC_CK(keep_pool_memory(device));
     cudaStream_t st;
     HMC_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     const size_t acc_bytes = (size_t)hmc_surface_acc_words(spec, sim.n_runs) * sizeof(int64_t);
@@ -822,11 +846,16 @@ int hmc_exact_batch_f64(const hmc_model* model, double s0, const double* step_ti
     e.key_run = key_run;
 
     HMC_CK(cudaSetDevice(device));
+    HMC_CK(keep_pool_memory(device));
     int dev = 0, sms = 148;
     HMC_CK(cudaGetDevice(&dev));
     HMC_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     long long blocks = (n + hmc::kExactThreads - 1) / hmc::kExactThreads;
-    const long long max_blocks = (long long)sms * 8;
+    // grid-stride kernel: one resident wave is enough, and the node cache
+    // (kExactCacheNodes doubles per thread) is sized by the grid
+    int per_sm = 0;
+    HMC_CK(hmc::exact_occupancy(&per_sm));
+    const long long max_blocks = (long long)sms * (per_sm > 0 ? per_sm : 4);
     const int grid = (int)(blocks < max_blocks ? blocks : max_blocks);
     const size_t threads = (size_t)grid * hmc::kExactThreads;
     cudaStream_t st;

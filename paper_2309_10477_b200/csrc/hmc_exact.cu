@@ -384,6 +384,10 @@ __global__ void __launch_bounds__(kExactThreads) exact_batch_kernel(const ExactA
     }
 }
 
+cudaError_t exact_occupancy(int* blocks_per_sm) {
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, exact_batch_kernel, kExactThreads, 0);
+}
+
 cudaError_t launch_exact(const ExactArgs& e, int grid, cudaStream_t s) {
     exact_batch_kernel<<<grid, kExactThreads, 0, s>>>(e);
     return cudaGetLastError();

@@ -82,6 +82,7 @@ struct ExactArgs {
 };
 
 cudaError_t launch_exact(const ExactArgs& e, int grid, cudaStream_t s);
+cudaError_t exact_occupancy(int* blocks_per_sm);
 
 // fp32 production kernel (hmc_fast.cu): tiles[run][tile][HMC_NW]
 cudaError_t launch_fast_greeks(const KernelArgs& a, double* d_tiles, long long n_tiles,
