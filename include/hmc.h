@@ -154,6 +154,19 @@ int hmc_reduce_chunks(const double* d_chunks, int32_t n_runs, int64_t n_chunks,
 int hmc_greeks(const hmc_model* model, const hmc_product* product,
                const hmc_sim* sim, double* h_out, int32_t device);
 
+/* Single-process multi-GPU one-call (the reference's multi-worker engine,
+ * engine.py:104-116, for C hosts that drive several GPUs themselves): the
+ * path axis is dealt in contiguous chunk-aligned slices over
+ * devices[0..n_devices) exactly as paper_2309_10477_b200.parallel.shard, each
+ * slice runs on its device's own stream concurrently, the chunk partials are
+ * copied in path order to devices[0] (peer copies over NVLink) and reduced
+ * there with the fixed-shape tree: bit-identical to hmc_greeks for any device
+ * list.  A device may appear more than once (several slices on one GPU).
+ * Synchronous, HOST output h_out[run][HMC_NW]. */
+int hmc_greeks_multi(const hmc_model* model, const hmc_product* product,
+                     const hmc_sim* sim, double* h_out, const int32_t* devices,
+                     int32_t n_devices);
+
 /* Reference backend call discretised_batch (_core.pyx:354-412) in fp64 on
  * the GPU: same key derivation, draw layout and arithmetic order.
  * uniforms: HOST (path_hi-path_lo, 2*n_steps) row-major or NULL (in-kernel

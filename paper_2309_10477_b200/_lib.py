@@ -40,7 +40,7 @@ PRECISION = {"fp32": 0, "fp64": 1}
 EXPORTS = (
     "hmc_abi_version", "hmc_last_error", "hmc_device_count",
     "hmc_chunks_in_slice", "hmc_workspace_bytes", "hmc_greeks_chunks",
-    "hmc_reduce_chunks", "hmc_greeks", "hmc_discretised_batch_f64",
+    "hmc_reduce_chunks", "hmc_greeks", "hmc_greeks_multi", "hmc_discretised_batch_f64",
     "hmc_sobol_init_directions", "hmc_root_key", "hmc_derive_key", "hmc_philox_check",
     "hmc_surface_acc_words", "hmc_surface_workspace_bytes", "hmc_surface_partials",
     "hmc_surface_finalize", "hmc_surface", "hmc_exact_batch_f64",
@@ -99,6 +99,7 @@ def _declare(L: ctypes.CDLL) -> None:
         "hmc_greeks_chunks": (ctypes.c_int, [pM, pP, pS, vp, vp, vp]),
         "hmc_reduce_chunks": (ctypes.c_int, [vp, i32, i64, vp, vp]),
         "hmc_greeks": (ctypes.c_int, [pM, pP, pS, pd, i32]),
+        "hmc_greeks_multi": (ctypes.c_int, [pM, pP, pS, pd, ctypes.POINTER(i32), i32]),
         "hmc_discretised_batch_f64": (ctypes.c_int, [pM, dbl, dbl, i32, i32, i64, i64, u64,
                                                      pd, ctypes.POINTER(i64), i64, pd, i32]),
         "hmc_sobol_init_directions": (ctypes.c_int, [ctypes.POINTER(i64), ctypes.POINTER(i64),

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <algorithm>
 #include <atomic>
 #include <utility>
 #include <vector>
@@ -595,6 +596,97 @@ int hmc_greeks(const hmc_model* model, const hmc_product* product, const hmc_sim
     }
     cudaError_t e2 = cudaStreamSynchronize(s);
     cudaStreamDestroy(s);
+    if (rc) return rc;
+    HMC_CK(e);
+    HMC_CK(e2);
+    return HMC_OK;
+}
+
+int hmc_greeks_multi(const hmc_model* model, const hmc_product* product, const hmc_sim* sim_in,
+                     double* h_out, const int32_t* devices, int32_t n_devices) {
+    if (!sim_in || !h_out) return fail(HMC_E_INVALID, "sim / h_out is NULL");
+    if (!devices || n_devices < 1 || n_devices > 1024) return fail(HMC_E_INVALID, "need 1..1024 devices");
+    hmc_sim sim = *sim_in;
+    sim.path_lo = 0;
+    sim.path_hi = sim.n_paths;
+    Prepared P;
+    int rc = prepare(model, product, &sim, P);  // validates the whole job before any device work
+    if (rc) return rc;
+    const long long C = P.n_chunks, R = sim.n_runs;
+    const size_t row = (size_t)HMC_NW * sizeof(double);
+
+    struct Part {
+        int dev = 0;
+        long long c_lo = 0, c_hi = 0;
+        hmc_sim sim{};
+        cudaStream_t st = nullptr;
+        cudaEvent_t done = nullptr;
+        char* buf = nullptr;
+    };
+    std::vector<Part> parts((size_t)n_devices);
+    const long long base = C / n_devices, extra = C % n_devices;
+    for (int r = 0; r < n_devices; ++r) {  // parallel.shard
+        Part& q = parts[r];
+        q.dev = devices[r];
+        q.c_lo = r * base + (r < extra ? r : extra);
+        q.c_hi = q.c_lo + base + (r < extra ? 1 : 0);
+        q.sim = sim;
+        q.sim.path_lo = std::min(q.c_lo * (long long)HMC_CHUNK, (long long)sim.n_paths);
+        q.sim.path_hi = std::min(q.c_hi * (long long)HMC_CHUNK, (long long)sim.n_paths);
+    }
+    // the gather buffer [run][C][HMC_NW] + the result live on devices[0]
+    const int root = devices[0];
+    HMC_CK(cudaSetDevice(root));
+    HMC_CK(keep_pool_memory(root));
+    cudaStream_t rs;
+    HMC_CK(cudaStreamCreateWithFlags(&rs, cudaStreamNonBlocking));
+    char* gbuf = nullptr;
+    const size_t gbytes = align_up((size_t)R * C * row) + (size_t)R * row;
+    // plain cudaMalloc: the peer copies of the other devices write into it
+    cudaError_t e = cudaMalloc((void**)&gbuf, gbytes);
+    double* g_chunks = (double*)gbuf;
+    double* g_out = (double*)(gbuf + align_up((size_t)R * C * row));
+
+    // launch every slice (asynchronous: the devices run concurrently)
+    for (Part& q : parts) {
+        if (e != cudaSuccess || rc != HMC_OK) break;
+        if (q.c_hi <= q.c_lo) continue;
+        if ((e = cudaSetDevice(q.dev)) != cudaSuccess) break;
+        if ((e = keep_pool_memory(q.dev)) != cudaSuccess) break;
+        if ((e = cudaStreamCreateWithFlags(&q.st, cudaStreamNonBlocking)) != cudaSuccess) break;
+        if ((e = cudaEventCreateWithFlags(&q.done, cudaEventDisableTiming)) != cudaSuccess) break;
+        const long long nc = q.c_hi - q.c_lo;
+        const size_t work = (size_t)hmc_workspace_bytes(&q.sim);
+        if ((e = cudaMallocAsync((void**)&q.buf, work + (size_t)R * nc * row, q.st)) != cudaSuccess) break;
+        double* loc = (double*)(q.buf + work);
+        rc = hmc_greeks_chunks(model, product, &q.sim, loc, q.buf, q.st);
+        if (rc != HMC_OK) break;
+        for (long long r = 0; r < R && e == cudaSuccess; ++r)  // run r's rows, in path order
+            e = cudaMemcpyPeerAsync(g_chunks + ((size_t)r * C + q.c_lo) * HMC_NW, root,
+                                    loc + (size_t)r * nc * HMC_NW, q.dev, (size_t)nc * row, q.st);
+        if (e == cudaSuccess) e = cudaEventRecord(q.done, q.st);
+    }
+    if (e == cudaSuccess && rc == HMC_OK) e = cudaSetDevice(root);
+    for (Part& q : parts)
+        if (e == cudaSuccess && rc == HMC_OK && q.done) e = cudaStreamWaitEvent(rs, q.done, 0);
+    if (e == cudaSuccess && rc == HMC_OK) {
+        rc = hmc_reduce_chunks(g_chunks, (int32_t)R, C, g_out, rs);
+        if (rc == HMC_OK) e = cudaMemcpyAsync(h_out, g_out, (size_t)R * row, cudaMemcpyDeviceToHost, rs);
+        if (e == cudaSuccess && rc == HMC_OK) e = cudaStreamSynchronize(rs);
+    }
+    // teardown on every path (errors included)
+    for (Part& q : parts) {
+        if (!q.st) continue;
+        cudaSetDevice(q.dev);
+        if (q.buf) cudaFreeAsync(q.buf, q.st);
+        cudaStreamSynchronize(q.st);
+        cudaStreamDestroy(q.st);
+        if (q.done) cudaEventDestroy(q.done);
+    }
+    cudaSetDevice(root);
+    cudaError_t e2 = cudaStreamSynchronize(rs);
+    if (gbuf) cudaFree(gbuf);
+    cudaStreamDestroy(rs);
     if (rc) return rc;
     HMC_CK(e);
     HMC_CK(e2);

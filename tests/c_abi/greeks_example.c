@@ -37,6 +37,17 @@ int main(int argc, char** argv) {
         const double var = (out[2 * q + 1] - out[2 * q] * mean) / (n_paths - 1);
         printf("%s %.17g %.6g\n", names[q], mean, sqrt(var > 0 ? var / n_paths : 0));
     }
+    /* the same job dealt over three slices (one GPU here, three streams):
+       bit-identical sums */
+    const int32_t devs[3] = {0, 0, 0};
+    double multi[HMC_NW];
+    if (hmc_greeks_multi(&m, &p, &s, multi, devs, 3) != HMC_OK) {
+        fprintf(stderr, "hmc_greeks_multi: %s\n", hmc_last_error());
+        return 1;
+    }
+    int same = 1;
+    for (int w = 0; w < HMC_NW; ++w) same &= multi[w] == out[w];
+    printf("multi_bit_identical %d\n", same);
     /* a usage error never touches the device */
     p.right = HMC_PUT;
     int rc = hmc_greeks(&m, &p, &s, out, 0);

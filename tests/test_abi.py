@@ -137,3 +137,18 @@ def test_host_digital_shifts_match_device_derivation():
         assert int(got[d]) == want
     pts = sobol.points(4, 1, 8, key_run=key)
     assert np.all((pts > 0) & (pts < 1))
+
+
+def test_greeks_multi_validates_before_device_work():
+    L = _lib.lib()
+    m, pr, sim, _keep = _job()
+    out = np.zeros(_lib.HMC_NW)
+    pd = ctypes.POINTER(ctypes.c_double)
+    devs = (ctypes.c_int32 * 2)(0, 0)
+    assert L.hmc_greeks_multi(ctypes.byref(m), ctypes.byref(pr), ctypes.byref(sim),
+                              out.ctypes.data_as(pd), None, 2) == _lib.HMC_E_INVALID
+    assert L.hmc_greeks_multi(ctypes.byref(m), ctypes.byref(pr), ctypes.byref(sim),
+                              out.ctypes.data_as(pd), devs, 0) == _lib.HMC_E_INVALID
+    m, pr, sim, _keep = _job(right=1)
+    assert L.hmc_greeks_multi(ctypes.byref(m), ctypes.byref(pr), ctypes.byref(sim),
+                              out.ctypes.data_as(pd), devs, 2) == _lib.HMC_E_UNSUPPORTED

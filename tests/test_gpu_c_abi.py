@@ -32,4 +32,31 @@ def test_plain_c_host(tmp_path):
     g = greeks(p, spec, SimConfig(scheme="milstein", n_paths=2**20, n_steps=252, n_runs=1, seed=42))
     for q in ("price", "delta", "rho", "gamma", "vega", "delta_fd", "rho_fd"):
         assert float(rows[q][0]) == pytest.approx(g[q].estimate, rel=1e-12, abs=1e-14), q
+    assert rows["multi_bit_identical"][0] == "1"
     assert rows["put_greeks_rc"][0] == "-4"
+
+
+@pytest.mark.parametrize("n_paths,n_runs,n_dev", [(70001, 3, 3), (40000, 2, 7), (2**20, 1, 2)])
+def test_greeks_multi_bit_identical(n_paths, n_runs, n_dev):
+    """hmc_greeks_multi deals chunk-aligned slices over a device list (here
+    the one GPU repeated: separate streams and buffers, the same code path
+    as distinct GPUs) and must reproduce hmc_greeks bit for bit, including
+    device lists longer than the chunk count (empty slices)."""
+    import ctypes
+    import numpy as np
+    from paper_2309_10477_b200 import _lib, engine
+    p = HestonParams(**BENCH_PARAMS)
+    spec = OptionSpec("asian_arithmetic", "call", 100.0, 1.0, 100.0, averaging_times=daily_fixings(1.0, 64))
+    job = engine.Job(p, spec, SimConfig(scheme="milstein", n_paths=n_paths, n_steps=64, n_runs=n_runs,
+                                        seed=5), True)
+    L = _lib.lib()
+    one = np.zeros((n_runs, _lib.HMC_NW))
+    multi = np.zeros((n_runs, _lib.HMC_NW))
+    pd = ctypes.POINTER(ctypes.c_double)
+    _lib.check(L.hmc_greeks(ctypes.byref(job.model), ctypes.byref(job.product), ctypes.byref(job.sim),
+                            one.ctypes.data_as(pd), 0))
+    devs = (ctypes.c_int32 * n_dev)(*([0] * n_dev))
+    _lib.check(L.hmc_greeks_multi(ctypes.byref(job.model), ctypes.byref(job.product), ctypes.byref(job.sim),
+                                  multi.ctypes.data_as(pd), devs, n_dev))
+    assert np.array_equal(one, multi)
+    assert np.all(one[:, 0] > 0)
