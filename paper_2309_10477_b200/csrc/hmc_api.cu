@@ -117,9 +117,12 @@ void build_bridge(int S, int n_sim, double dt, Prepared& P) {
             P.bs64[k] = {1.0 / (left + 1.0), std::sqrt(dt * left / (left + 1.0)), j, k < b[j] ? 1 : 0};
         }
     P.bn32.clear();
-    for (const auto& n : P.bn64) P.bn32.push_back({(float)n.a, (float)n.sd, n.m, n.l | (n.r << 16)});
+    // fp32 tables: the kernel's Sobol normals come as z / sqrt(2) (hmc_path32.cuh
+    // sobol_normal_u), so the noise coefficients carry the sqrt(2)
+    const double r2 = std::sqrt(2.0);
+    for (const auto& n : P.bn64) P.bn32.push_back({(float)n.a, (float)(n.sd * r2), n.m, n.l | (n.r << 16)});
     P.bs32.clear();
-    for (const auto& st : P.bs64) P.bs32.push_back({(float)st.alpha, (float)st.beta});
+    for (const auto& st : P.bs64) P.bs32.push_back({(float)st.alpha, (float)(st.beta * r2)});
 }
 
 int check_model(const hmc_model* m) {

@@ -80,7 +80,7 @@ struct SobolLane {
     int which;          // this lane's block
     uint32_t jl;        // Gray code of the lane part
     unsigned long long key_run;
-    float half;         // 0.5: cell midpoints of shifted points
+    float hx, ht;       // half 2^-29, half 2^-30 (half = 0.5: cell midpoints of shifted points)
 
     __device__ __forceinline__ SobolLane(int run, long long p, const KernelArgs& a) {
         // scrambled (randomised QMC): every run re-uses points 1..N under its own shifts
@@ -93,7 +93,9 @@ struct SobolLane {
         const uint32_t c = n & 31u;
         jl = c ^ (c >> 1);
         key_run = derive(a.root_key, (unsigned long long)run);
-        half = a.sobol_scramble ? 0.5f : 0.0f;
+        const float half = a.sobol_scramble ? 0.5f : 0.0f;
+        hx = half * 1.86264514923095703125e-09f;
+        ht = half * 9.31322574615478515625e-10f;
     }
 };
 
@@ -136,22 +138,22 @@ __device__ __forceinline__ void sobol_refill(Tab& tab, int q0, int m, const Sobo
     __syncthreads();
 }
 
-// the two standard normals of pair q of the loaded chunk
+// the two standard normals (divided by sqrt(2)) of pair q of the loaded chunk
 template <class Tab>
 __device__ __forceinline__ void sobol_pair(const Tab& tab, int q, const SobolLane& sl,
                                            float& za, float& zb) {
     const uint2 t = tab.T[q][sl.jl];
     const uint2 u = tab.U[threadIdx.x >> 5][sl.which][q];
-    za = sobol_normal(t.x ^ u.x, sl.half);
-    zb = sobol_normal(t.y ^ u.y, sl.half);
+    za = sobol_normal_u(t.x ^ u.x, sl.hx, sl.ht);
+    zb = sobol_normal_u(t.y ^ u.y, sl.hx, sl.ht);
 }
 
 template <int FIX, bool GREEKS>
 __device__ __forceinline__ void sobol_paths(PathState32& st, int run, long long p, const KernelArgs& a) {
     __shared__ SobolTables tab;
     const SobolLane sl(run, p, a);
-    const float c1 = a.f_sqdt * a.f_log2e;
-    const float cs = a.f_sigma * a.f_sqdt;
+    const float c1 = kSqrt2f * a.f_sqdt * a.f_log2e;  // sobol_pair returns z / sqrt(2)
+    const float cs = kSqrt2f * a.f_sigma * a.f_sqdt;
 
 #pragma unroll 1
     for (int k0 = 1; k0 <= a.n_sim; k0 += kSobolSteps) {

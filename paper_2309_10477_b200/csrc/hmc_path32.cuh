@@ -22,9 +22,6 @@
 #ifndef HMC_PIPELINE_RNG
 #define HMC_PIPELINE_RNG 0   // generate step pair j+1's Philox block during pair j
 #endif
-#ifndef HMC_SOBOL_NOI2F
-#define HMC_SOBOL_NOI2F 0    // Sobol quantile without I2F conversions (FMA/ALU only)
-#endif
 #ifndef HMC_EX2_DELTA
 #define HMC_EX2_DELTA 0      // bumped trajectories' 2^L from the base one (guarded)
 #endif
@@ -189,24 +186,16 @@ __device__ __forceinline__ void box_muller(uint32_t xr, uint32_t xa, const Kerne
 // Giles' single-precision erfinv, z = sqrt(2) erfinv(2u - 1), with 4u(1-u)
 // formed from the distance to the nearer end so the tails keep precision.
 // half = 0 for the reference's unscrambled points (x >= 1 always); half = 1/2
-// for digitally shifted points, where x = 0 can occur.
-__device__ __forceinline__ float sobol_normal(uint32_t x, float half) {
+// for digitally shifted points, where x = 0 can occur.  Returns z / sqrt(2)
+// (callers fold sqrt(2) into their constants); hx = half 2^-29 and
+// ht = half 2^-30 are loop invariants of the caller.
+__device__ __forceinline__ float sobol_normal_u(uint32_t x, float hx, float ht) {
     const uint32_t t = min(x, (1u << 30) - x);              // min(u, 1-u) 2^30 (- half)
-#if HMC_SOBOL_NOI2F
-    // int -> float without the XU conversion pipe: 2u - 1 from the top 23
-    // bits (exponent trick), and t exactly as th 2^15 + tl with each 15-bit
-    // half placed in a 2^23-biased mantissa
-    const float u23 = __uint_as_float((x >> 7) | 0x3f800000u) - 1.0f;
-    const float xs = fmaf(u23, 2.0f, fmaf(half, 1.86264514923095703125e-09f, -1.0f));
-    const float fh = __uint_as_float(0x4B000000u | (t >> 15)) - 8388608.0f;
-    const float fl = __uint_as_float(0x4B000000u | (t & 0x7FFFu)) - 8388608.0f;
-    const float tf = (fmaf(fh, 32768.0f, fl) + half) * 9.31322574615478515625e-10f;
-#else
     const int m = (int)(2u * x) - (1 << 30);                // (2u - 1) 2^30 - 2 half
-    const float xs = fmaf((float)m, 9.31322574615478515625e-10f, half * 1.86264514923095703125e-09f);
-    const float tf = ((float)t + half) * 9.31322574615478515625e-10f;
-#endif
-    float w = -0.69314718055994530942f * lg2a(4.0f * tf * (1.0f - tf));
+    const float xs = fmaf((float)m, 9.31322574615478515625e-10f, hx);
+    const float tf = fmaf((float)t, 9.31322574615478515625e-10f, ht);
+    // w = -ln(4 tf (1 - tf)) = -ln2 (lg2(tf (1 - tf)) + 2)
+    float w = fmaf(lg2a(tf * (1.0f - tf)), -0.69314718055994530942f, -1.38629436111989061883f);
     float p;
     if (w < 5.0f) {
         w = w - 2.5f;
@@ -231,8 +220,10 @@ __device__ __forceinline__ float sobol_normal(uint32_t x, float half) {
         p = fmaf(p, w, 1.00167406f);
         p = fmaf(p, w, 2.83297682f);
     }
-    return 1.41421356237309504880f * p * xs;
+    return p * xs;
 }
+
+constexpr float kSqrt2f = 1.41421356237309504880f;
 
 struct PathState32 {
     float v0, L0, A0;  // base trajectory
