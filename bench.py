@@ -78,7 +78,7 @@ def secondary_workloads(reps: int = 3) -> dict:
                                                sobol_bridge=16, n_paths=2**22, n_steps=252,
                                                n_runs=1, seed=7)),
             2**22 * 252),
-        "exact_bk_european_price_2^17": (
+        "exact_bk_european_full_greeks_2^17": (
             lambda: greeks(p, euro, SimConfig(scheme="exact", n_paths=2**17, n_steps=1, n_runs=1,
                                               seed=7)), 2**17),
         "c5_surface_64Kx8T_euro+asian_full_greeks_2^22x504": (
