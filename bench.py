@@ -210,6 +210,17 @@ def cpu_reference_pass(n_paths: int, workers: int) -> float:
     return time.perf_counter() - t0
 
 
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline_block(n_paths: int = 0) -> dict:
     import oracle
     workers = os.cpu_count() or 1
@@ -220,10 +231,11 @@ def cpu_baseline_block(n_paths: int = 0) -> dict:
                 "sample": "oracle/_ref missing; not timed"}
     cpu_reference_pass(2 ** 12, workers)  # warm the pool / page in
     secs = cpu_reference_pass(n_paths, workers)
+    one = cpu_reference_pass(4096, 1)      # one reference job on one core
     return {"value": n_paths * N_STEPS / secs, "unit": UNIT, "cores": workers, "kind": kind,
             "sample": f"{n_paths} paths x {N_STEPS} steps, Asian daily fixings, full Greeks as "
                       f"greeks() + 4 CRN bumped price() passes, {secs:.2f} s wall",
-            "seconds": secs}
+            "seconds": secs, "per_core_value": 4096 * N_STEPS / one, "cpu_model": _cpu_model()}
 
 
 def run_reference(args) -> None:
@@ -236,6 +248,7 @@ def run_reference(args) -> None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
     n = max(2 ** 15, 2 * 4096 * workers)   # >= 2 reference jobs per worker
+    n = int(os.environ.get("HMC_BENCH_REF_PATHS", n))  # tests: a smaller sample
     for _ in range(args.warmup):
         cpu_reference_pass(n, workers)
     times = [cpu_reference_pass(n, workers) for _ in range(args.steps)]

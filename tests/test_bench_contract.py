@@ -1,0 +1,52 @@
+"""bench.py's JSON-line contract on the CPU: the reference arm runs and
+prints the required keys, non-zero ranks stay silent, and the B200 arm
+fails loudly (no CPU fallback) when no GPU is visible."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+import oracle
+
+
+def _run(args, **env):
+    e = dict(os.environ, **env)
+    return subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True,
+                          text=True, env=e, cwd=ROOT, timeout=600)
+
+
+@pytest.mark.skipif(oracle.ref_core() is None, reason="oracle/_ref (reference kernel) not built")
+def test_reference_arm_line():
+    r = _run(["--impl", "reference", "--steps", "1", "--warmup", "0"], HMC_BENCH_REF_PATHS="4096")
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "impl", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
+    assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["value"] == d["value"]
+    assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}
+    assert d["config"]["workload"]
+
+
+def test_reference_arm_silent_on_other_ranks():
+    r = _run(["--impl", "reference", "--steps", "1", "--warmup", "0"], RANK="1", WORLD_SIZE="2")
+    assert r.returncode == 0
+    assert r.stdout.strip() == ""
+
+
+def test_b200_arm_fails_loudly_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is visible")
+    r = _run(["--steps", "1", "--warmup", "3"])
+    assert r.returncode != 0
+    assert '"value"' not in r.stdout
