@@ -25,6 +25,8 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2",
           f"-I{os.path.join(ROOT, 'include')}"]
 UNITS = {
     "hmc_api.cu": [],
+    "hmc_api_surface.cu": [],
+    "hmc_api_exact.cu": [],
     "hmc_fast.cu": [],
     "hmc_replay.cu": ["-fmad=false"],
     "hmc_surface.cu": [],

@@ -320,7 +320,10 @@ __device__ double sample_iv(double kappa, double theta, double sigma, double dof
 
 }  // namespace
 
-__global__ void __launch_bounds__(kExactThreads) exact_batch_kernel(const ExactArgs e) {
+#ifndef HMC_EXACT_MINB
+#define HMC_EXACT_MINB 1
+#endif
+__global__ void __launch_bounds__(kExactThreads, HMC_EXACT_MINB) exact_batch_kernel(const ExactArgs e) {
     const long long n = e.path_hi - e.path_lo;
     const long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long stride = (long long)gridDim.x * blockDim.x;
