@@ -451,6 +451,7 @@ int hmc_greeks(const hmc_model* model, const hmc_product* product, const hmc_sim
     Prepared P;
     int rc = prepare(model, product, &sim, P);
     if (rc) return rc;
+    const DeviceGuard keep_device;
     HMC_CK(cudaSetDevice(device));
     HMC_CK(keep_pool_memory(device));
     cudaStream_t s;
@@ -513,6 +514,7 @@ int hmc_greeks_multi(const hmc_model* model, const hmc_product* product, const h
     }
     // the gather buffer [run][C][HMC_NW] + the result live on devices[0]
     const int root = devices[0];
+    const DeviceGuard keep_device;
     HMC_CK(cudaSetDevice(root));
     HMC_CK(keep_pool_memory(root));
     cudaStream_t rs;
@@ -601,6 +603,7 @@ int hmc_discretised_batch_f64(const hmc_model* model, double s0, double T, int32
     for (int64_t i = 0; i < n_avg; ++i) fix[avg_idx[i]] = 1;
     build_steps(n_steps, T, 0.0, s0, model->r, fix.data(), P);
 
+    const DeviceGuard keep_device;
     HMC_CK(cudaSetDevice(device));
     HMC_CK(keep_pool_memory(device));
     cudaStream_t s;
@@ -631,6 +634,7 @@ int hmc_discretised_batch_f64(const hmc_model* model, double s0, double T, int32
 
 int hmc_philox_check(const uint32_t* ctr, int32_t n, uint32_t* out, int32_t device) {
     if (!ctr || !out || n < 1) return fail(HMC_E_INVALID, "bad philox check arguments");
+    const DeviceGuard keep_device;
     HMC_CK(cudaSetDevice(device));
     uint4 *d_c = nullptr, *d_o = nullptr;
     HMC_CK(cudaMalloc((void**)&d_c, (size_t)n * sizeof(uint4)));

@@ -40,6 +40,7 @@ int hmc_exact_batch_f64(const hmc_model* model, double s0, const double* step_ti
     e.path_hi = path_hi;
     e.key_run = key_run;
 
+    const DeviceGuard keep_device;
     HMC_CK(cudaSetDevice(device));
     HMC_CK(keep_pool_memory(device));
     int dev = 0, sms = 148;

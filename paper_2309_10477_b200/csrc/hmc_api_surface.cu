@@ -224,6 +224,7 @@ int hmc_surface(const hmc_model* model, const hmc_surface_spec* spec, const hmc_
     SurfPrepared S;
     int rc = prepare_surface(model, spec, &sim, S);
     if (rc) return rc;
+    const DeviceGuard keep_device;
     HMC_CK(cudaSetDevice(device));
     HMC_CK(keep_pool_memory(device));
     cudaStream_t st;

@@ -31,6 +31,23 @@ int fail(int code, const std::string& msg);
                         std::string(#expr) + ": " + cudaGetErrorString(e_));          \
     } while (0)
 
+// The one-call entry points select their device; restore the caller's
+// current device on return (a library call must not move it).
+struct DeviceGuard {
+    int prev = -1;
+    DeviceGuard() {
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            prev = -1;
+            cudaGetLastError();
+        }
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 // keep freed blocks in the device's default stream-ordered pool (hmc_api.cu)
 cudaError_t keep_pool_memory(int dev);
 
