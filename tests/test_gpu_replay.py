@@ -68,6 +68,33 @@ class TestKnownAnswers:
         out = cuda_backend.discretised_batch(params, 100.0, 1.0, 1, False, 0, 4, 0, u, np.array([1]))
         assert out[:, 0] == pytest.approx(100.0 * math.exp(params.r - 0.5 * params.v0), rel=1e-14)
 
+    def test_multi_step_drift_only(self, params):
+        """z1 = z2 = 0 (uniforms 1/2): the variance follows the deterministic
+        recursion and S the drift exp((r - v/2) dt) (reference
+        tests/test_schemes.py:34-46), Euler and Milstein."""
+        n, T = 8, 1.0
+        dt = T / n
+        u = np.full((3, 2 * n), 0.5)
+        for milstein in (False, True):
+            out = cuda_backend.discretised_batch(params, 100.0, T, n, milstein, 0, 3, 0, u, np.array([n]))
+            s, v = 100.0, params.v0
+            for _ in range(n):
+                s = s * math.exp((params.r - 0.5 * v) * dt)
+                vn = v + params.kappa * (params.theta - v) * dt
+                if milstein:
+                    vn += 0.25 * params.sigma ** 2 * dt * (0.0 - 1.0)
+                v = max(vn, 0.0)
+            np.testing.assert_allclose(out[:, 0], s, rtol=1e-14)
+
+    def test_euler_equals_milstein_as_sigma_vanishes(self):
+        """reference tests/test_schemes.py:80-88: the Milstein correction is
+        O(sigma^2), so with sigma -> 0 both schemes give the same paths."""
+        p = HestonParams(**{**DEFAULT_PARAMS, "sigma": 1e-7})
+        kr = oracle.derive_key(oracle.root_key(3), 0)
+        a = cuda_backend.discretised_batch(p, 100.0, 1.0, 64, False, 0, 512, kr, None, np.array([64]))
+        b = cuda_backend.discretised_batch(p, 100.0, 1.0, 64, True, 0, 512, kr, None, np.array([64]))
+        np.testing.assert_allclose(a, b, rtol=1e-10)
+
     def test_milstein_equals_euler_when_z2_is_one(self):
         p = HestonParams(**{**DEFAULT_PARAMS, "rho": 0.0})
         u = np.array([[0.31, float(ndtr(1.0))]] * 8)
