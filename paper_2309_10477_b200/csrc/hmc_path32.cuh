@@ -16,6 +16,9 @@
 #ifndef HMC_EX2_POLY
 #define HMC_EX2_POLY 0
 #endif
+#ifndef HMC_SOBOL_VOTE
+#define HMC_SOBOL_VOTE 1     // Sobol quantile: warp-voted tail branch (all 32 lanes must be active)
+#endif
 #ifndef HMC_SQRT_RSQ
 #define HMC_SQRT_RSQ 0
 #endif
@@ -197,6 +200,37 @@ __device__ __forceinline__ float sobol_normal_u(uint32_t x, float hx, float ht) 
     // w = -ln(4 tf (1 - tf)) = -ln2 (lg2(tf (1 - tf)) + 2)
     float w = fmaf(lg2a(tf * (1.0f - tf)), -0.69314718055994530942f, -1.38629436111989061883f);
     float p;
+#if HMC_SOBOL_VOTE
+    // central branch for every lane; the tail branch (|2u - 1| > 0.9966,
+    // 0.3 % of draws) only in warps where a lane needs it: a uniform vote
+    // instead of a divergent if/else around both polynomials
+    {
+        const float wc = w - 2.5f;
+        p = 2.81022636e-08f;
+        p = fmaf(p, wc, 3.43273939e-07f);
+        p = fmaf(p, wc, -3.5233877e-06f);
+        p = fmaf(p, wc, -4.39150654e-06f);
+        p = fmaf(p, wc, 0.00021858087f);
+        p = fmaf(p, wc, -0.00125372503f);
+        p = fmaf(p, wc, -0.00417768164f);
+        p = fmaf(p, wc, 0.246640727f);
+        p = fmaf(p, wc, 1.50140941f);
+    }
+    if (__any_sync(0xffffffffu, w >= 5.0f)) {
+        const float wt = sqrta(w) - 3.0f;
+        float q = -0.000200214257f;
+        q = fmaf(q, wt, 0.000100950558f);
+        q = fmaf(q, wt, 0.00134934322f);
+        q = fmaf(q, wt, -0.00367342844f);
+        q = fmaf(q, wt, 0.00573950773f);
+        q = fmaf(q, wt, -0.0076224613f);
+        q = fmaf(q, wt, 0.00943887047f);
+        q = fmaf(q, wt, 1.00167406f);
+        q = fmaf(q, wt, 2.83297682f);
+        p = w >= 5.0f ? q : p;
+    }
+#else
+    float p;
     if (w < 5.0f) {
         w = w - 2.5f;
         p = 2.81022636e-08f;
@@ -220,6 +254,7 @@ __device__ __forceinline__ float sobol_normal_u(uint32_t x, float hx, float ht) 
         p = fmaf(p, w, 1.00167406f);
         p = fmaf(p, w, 2.83297682f);
     }
+#endif
     return p * xs;
 }
 
