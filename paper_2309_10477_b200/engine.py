@@ -29,7 +29,7 @@ import numpy as np
 
 from . import _lib, parallel, sobol
 from .errors import DeviceError, UnsupportedProduct
-from .model import GridSpec, HestonParams, McSummary, OptionSpec, SimConfig, averaging_indices
+from .model import GridSpec, HestonParams, McSummary, OptionSpec, SimConfig, fixing_index_array
 
 _QNAMES = _lib.QUANTITIES
 
@@ -52,8 +52,8 @@ def _validate(spec: OptionSpec, config: SimConfig, want_greeks: bool) -> list[in
         return []
     grid = GridSpec(maturity=spec.maturity, n_steps=config.n_steps)
     if spec.is_asian:
-        return averaging_indices(grid, spec.averaging_times)
-    return [config.n_steps]
+        return fixing_index_array(grid, spec.averaging_times)
+    return np.array([config.n_steps], dtype=np.int64)
 
 
 def bump_sizes(params: HestonParams, spec: OptionSpec, config: SimConfig) -> tuple[float, float, float, float]:
