@@ -235,6 +235,16 @@ int hmc_exact_batch_f64(const hmc_model* model, double s0, const double* step_ti
                         int64_t path_hi, uint64_t key_run, const double* uniforms,
                         double* out, int32_t device);
 
+/* The same for n_runs independent runs in ONE launch (the reference engine
+ * calls exact_batch once per run and 4096-path job, engine.py:93-116):
+ * run r uses key_runs[r] (derive_key(root_key(seed), r)); uniforms: HOST
+ * [n_runs][path_hi-path_lo][3*n_steps] or NULL; out: HOST
+ * [n_runs][path_hi-path_lo][3].  Per-path values equal hmc_exact_batch_f64's. */
+int hmc_exact_runs_f64(const hmc_model* model, double s0, const double* step_times,
+                       int32_t n_steps, const int64_t* avg_flags, int64_t path_lo,
+                       int64_t path_hi, const uint64_t* key_runs, int32_t n_runs,
+                       const double* uniforms, double* out, int32_t device);
+
 /* Joe-Kuo direction numbers as used by scipy.stats.qmc.Sobol(scramble=False)
  * (30 bits): poly[dim], vinit[dim][18] from scipy's
  * _sobol_direction_numbers.npz -> v_out[30][dim] (HOST).  Point n of the

@@ -43,7 +43,7 @@ EXPORTS = (
     "hmc_reduce_chunks", "hmc_greeks", "hmc_greeks_multi", "hmc_discretised_batch_f64",
     "hmc_sobol_init_directions", "hmc_root_key", "hmc_derive_key", "hmc_philox_check",
     "hmc_surface_acc_words", "hmc_surface_workspace_bytes", "hmc_surface_partials",
-    "hmc_surface_finalize", "hmc_surface", "hmc_exact_batch_f64",
+    "hmc_surface_finalize", "hmc_surface", "hmc_exact_batch_f64", "hmc_exact_runs_f64",
 )
 HMC_SURF_MAX_STRIKES = 128
 HMC_SURF_MAX_MATS = 32
@@ -114,6 +114,8 @@ def _declare(L: ctypes.CDLL) -> None:
         "hmc_surface": (ctypes.c_int, [pM, ctypes.POINTER(SurfaceSpec), pS, pd, i32]),
         "hmc_exact_batch_f64": (ctypes.c_int, [pM, dbl, pd, i32, ctypes.POINTER(i64), i64, i64, u64,
                                                pd, pd, i32]),
+        "hmc_exact_runs_f64": (ctypes.c_int, [pM, dbl, pd, i32, ctypes.POINTER(i64), i64, i64,
+                                              ctypes.POINTER(u64), i32, pd, pd, i32]),
         "hmc_root_key": (u64, [u64]),
         "hmc_derive_key": (u64, [u64, u64]),
     }

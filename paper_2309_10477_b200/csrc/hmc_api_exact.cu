@@ -1,5 +1,5 @@
 // hmc_api_exact.cu -- C ABI of the Broadie-Kaya exact scheme
-// (hmc_exact_batch_f64) and the Sobol direction-number construction
+// (hmc_exact_batch_f64, hmc_exact_runs_f64) and the Sobol direction-number construction
 // (hmc_sobol_init_directions).
 #include <cuda_runtime.h>
 
@@ -13,9 +13,10 @@ using namespace hmc_host;
 
 extern "C" {
 
-int hmc_exact_batch_f64(const hmc_model* model, double s0, const double* step_times,
-                        int32_t n_steps, const int64_t* avg_flags, int64_t path_lo, int64_t path_hi,
-                        uint64_t key_run, const double* uniforms, double* out, int32_t device) {
+int hmc_exact_runs_f64(const hmc_model* model, double s0, const double* step_times,
+                       int32_t n_steps, const int64_t* avg_flags, int64_t path_lo, int64_t path_hi,
+                       const uint64_t* key_runs, int32_t n_runs, const double* uniforms, double* out,
+                       int32_t device) {
     int rc = check_model(model);
     if (rc) return rc;
     if (!(s0 > 0.0) || n_steps < 1 || !step_times || !avg_flags)
@@ -23,8 +24,10 @@ int hmc_exact_batch_f64(const hmc_model* model, double s0, const double* step_ti
     for (int k = 0; k < n_steps; ++k)
         if (!(step_times[k + 1] > step_times[k])) return fail(HMC_E_INVALID, "step_times must increase");
     if (path_hi < path_lo) return fail(HMC_E_INVALID, "path_hi < path_lo");
+    if (n_runs < 1 || !key_runs) return fail(HMC_E_INVALID, "need n_runs >= 1 and key_runs");
     const long long n = path_hi - path_lo;
     if (n == 0) return HMC_OK;
+    const long long rows = n * n_runs;
     if (!out) return fail(HMC_E_INVALID, "out is NULL");
     long long n_dates = 0;
     for (int k = 0; k < n_steps; ++k) n_dates += avg_flags[k] ? 1 : 0;
@@ -38,7 +41,7 @@ int hmc_exact_batch_f64(const hmc_model* model, double s0, const double* step_ti
     e.n_dates = n_dates;
     e.path_lo = path_lo;
     e.path_hi = path_hi;
-    e.key_run = key_run;
+    e.n_runs = n_runs;
 
     const DeviceGuard keep_device;
     HMC_CK(cudaSetDevice(device));
@@ -46,7 +49,7 @@ int hmc_exact_batch_f64(const hmc_model* model, double s0, const double* step_ti
     int dev = 0, sms = 148;
     HMC_CK(cudaGetDevice(&dev));
     HMC_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    long long blocks = (n + hmc::kExactThreads - 1) / hmc::kExactThreads;
+    long long blocks = (rows + hmc::kExactThreads - 1) / hmc::kExactThreads;
     // grid-stride kernel: one resident wave is enough, and the node cache
     // (kExactCacheNodes doubles per thread) is sized by the grid
     int per_sm = 0;
@@ -57,10 +60,12 @@ int hmc_exact_batch_f64(const hmc_model* model, double s0, const double* step_ti
     cudaStream_t st;
     HMC_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     const size_t tb = ((size_t)n_steps + 1) * sizeof(double), fb = (size_t)n_steps * sizeof(long long);
-    const size_t ub = uniforms ? (size_t)n * 3 * n_steps * sizeof(double) : 0;
-    const size_t ob = (size_t)n * 3 * sizeof(double);
+    const size_t ub = uniforms ? (size_t)rows * 3 * n_steps * sizeof(double) : 0;
+    const size_t ob = (size_t)rows * 3 * sizeof(double);
     const size_t sb = (size_t)hmc::kExactCacheNodes * threads * sizeof(double);
-    const size_t total = align_up(tb) + align_up(fb) + align_up(ub) + align_up(ob) + align_up(sb) + 256;
+    const size_t kb = (size_t)n_runs * sizeof(uint64_t);
+    const size_t total = align_up(tb) + align_up(fb) + align_up(ub) + align_up(ob) + align_up(sb) +
+                         align_up(kb) + 256;
     char* buf = nullptr;
     int h_err = 0;
     cudaError_t ce = cudaMallocAsync((void**)&buf, total, st);
@@ -71,12 +76,15 @@ int hmc_exact_batch_f64(const hmc_model* model, double s0, const double* step_ti
         double* d_u = uniforms ? (double*)(buf + off) : nullptr; off += align_up(ub);
         double* d_o = (double*)(buf + off); off += align_up(ob);
         double* d_s = (double*)(buf + off); off += align_up(sb);
+        unsigned long long* d_k = (unsigned long long*)(buf + off); off += align_up(kb);
         int* d_err = (int*)(buf + off);
         std::vector<long long> flags(avg_flags, avg_flags + n_steps);
         ce = cudaMemcpyAsync(d_t, step_times, tb, cudaMemcpyHostToDevice, st);
         if (ce == cudaSuccess) ce = cudaMemcpyAsync(d_f, flags.data(), fb, cudaMemcpyHostToDevice, st);
         if (ce == cudaSuccess && uniforms) ce = cudaMemcpyAsync(d_u, uniforms, ub, cudaMemcpyHostToDevice, st);
+        if (ce == cudaSuccess) ce = cudaMemcpyAsync(d_k, key_runs, kb, cudaMemcpyHostToDevice, st);
         if (ce == cudaSuccess) ce = cudaMemsetAsync(d_err, 0, sizeof(int), st);
+        e.key_runs = d_k;
         e.times = d_t;
         e.flags = d_f;
         e.uniforms = d_u;
@@ -100,6 +108,13 @@ int hmc_exact_batch_f64(const hmc_model* model, double s0, const double* step_ti
         case 3: return fail(HMC_E_QUAD, "characteristic-function tail did not fall below tolerance");
         default: return fail(HMC_E_ROOT, "CDF inversion failed to reach tolerance");
     }
+}
+
+int hmc_exact_batch_f64(const hmc_model* model, double s0, const double* step_times,
+                        int32_t n_steps, const int64_t* avg_flags, int64_t path_lo, int64_t path_hi,
+                        uint64_t key_run, const double* uniforms, double* out, int32_t device) {
+    return hmc_exact_runs_f64(model, s0, step_times, n_steps, avg_flags, path_lo, path_hi, &key_run, 1,
+                              uniforms, out, device);
 }
 
 // Bratley-Fox / Joe-Kuo recurrence on the m-values, then the 2^(bits-1-b)

@@ -332,9 +332,11 @@ __global__ void __launch_bounds__(kExactThreads, HMC_EXACT_MINB) exact_batch_ker
     nc.stride = stride;
     nc.cap = kExactCacheNodes;
     const bool point_mass = e.sigma < 1e-4 * e.kappa;
-    for (long long i = slot; i < n; i += stride) {
+    const long long total = n * e.n_runs;  // (run, path) pairs; row i of uniforms / out
+    for (long long i = slot; i < total; i += stride) {
         int err = kErrNone;
-        const unsigned long long key_path = derive(e.key_run, (unsigned long long)(e.path_lo + i));
+        const long long run = i / n, p = i - run * n;
+        const unsigned long long key_path = derive(e.key_runs[run], (unsigned long long)(e.path_lo + p));
         const unsigned long long main_key = derive(key_path, 0ULL);
         const unsigned long long gamma_root = derive(key_path, 1ULL);
         double ln_s = log(e.s0), v = e.v0, price_sum = 0.0, tw_sum = 0.0;

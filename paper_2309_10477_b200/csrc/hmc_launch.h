@@ -74,9 +74,10 @@ struct ExactArgs {
     int n_steps;
     long long n_dates;
     long long path_lo, path_hi;
-    unsigned long long key_run;
-    const double* uniforms;  // [n][3 n_steps] or null
-    double* out;             // [n][3]
+    const unsigned long long* key_runs;  // [n_runs] per-run stream keys (device)
+    int n_runs;
+    const double* uniforms;  // [n_runs][n][3 n_steps] or null
+    double* out;             // [n_runs][n][3]
     double* scratch;         // [kExactCacheNodes][grid threads]
     int* err_flag;           // max reference error code seen
 };

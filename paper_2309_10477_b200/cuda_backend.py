@@ -93,3 +93,32 @@ def exact_batch(params, s0: float, step_times, avg_flags, path_lo: int, path_hi:
         out.ctypes.data_as(pd), _device())
     _lib.check(rc)
     return out
+
+
+def exact_runs(params, s0: float, step_times, avg_flags, path_lo: int, path_hi: int, key_runs,
+               uniforms) -> np.ndarray:
+    """``exact_batch`` for several runs in one launch: run r uses
+    ``key_runs[r]``; ``uniforms`` is None or (n_runs, n, 3*n_steps).
+    Returns (n_runs, n, 3) -- each run's rows equal ``exact_batch``'s."""
+    times = np.ascontiguousarray(step_times, dtype=np.float64)
+    flags = np.ascontiguousarray(avg_flags, dtype=np.int64)
+    n_steps = times.size - 1
+    if flags.size != n_steps:
+        raise ValueError("avg_flags needs one flag per step")
+    keys = np.ascontiguousarray([int(k) & (2**64 - 1) for k in key_runs], dtype=np.uint64)
+    n = int(path_hi) - int(path_lo)
+    out = np.empty((keys.size, max(n, 0), 3))
+    u = None
+    if uniforms is not None:
+        u = np.ascontiguousarray(uniforms, dtype=np.float64)
+        if u.shape != (keys.size, n, 3 * n_steps):
+            raise ValueError("uniforms must be (n_runs, path_hi - path_lo, 3 * n_steps)")
+    m = _lib.Model(params.kappa, params.theta, params.sigma, params.rho, params.r, params.v0)
+    pd = ctypes.POINTER(ctypes.c_double)
+    rc = _lib.lib().hmc_exact_runs_f64(
+        ctypes.byref(m), float(s0), times.ctypes.data_as(pd), n_steps,
+        flags.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), int(path_lo), int(path_hi),
+        keys.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), keys.size,
+        None if u is None else u.ctypes.data_as(pd), out.ctypes.data_as(pd), _device())
+    _lib.check(rc)
+    return out

@@ -90,34 +90,44 @@ def execute(params: HestonParams, spec: OptionSpec, config: SimConfig, want_gree
     from . import _lib
     key_root = _lib.lib().hmc_root_key(config.seed & (2**64 - 1))
     out = np.zeros((config.n_runs, 14))
-    for run in range(config.n_runs):
-        key_run = _lib.lib().hmc_derive_key(key_root, run)
+    variants = [params]
+    if want_greeks:
+        variants += [p_up, p_dn] + ([p_rp, p_rm] if spec.is_asian else [])
+    # runs go to the GPU in batches (one launch per model variant and batch);
+    # a batch is bounded so the host buffers stay ~<= 256 MB
+    per_run_bytes = max(sl.n_paths, 1) * 8 * (3 * len(variants) + (3 * n_steps if config.sampler == "sobol" else 0))
+    batch = max(1, min(config.n_runs, (256 << 20) // per_run_bytes))
+    for r0 in range(0, config.n_runs, batch):
+        runs = range(r0, min(config.n_runs, r0 + batch))
+        key_runs = [_lib.lib().hmc_derive_key(key_root, run) for run in runs]
         u = None
-        if config.sampler == "sobol":  # engine.py:97-101
+        if config.sampler == "sobol" and sl.n_paths > 0:  # engine.py:97-101
             if config.sobol_scramble:      # randomised QMC: points 1..N, per-run shifts
-                u = sobol.points(3 * n_steps, 1 + sl.path_lo, sl.n_paths, key_run=key_run)
+                u = np.stack([sobol.points(3 * n_steps, 1 + sl.path_lo, sl.n_paths, key_run=k)
+                              for k in key_runs])
             else:
-                u = sobol.points(3 * n_steps, 1 + run * config.n_paths + sl.path_lo, sl.n_paths)
-        partials = np.zeros((len(jobs), 14))
+                u = np.stack([sobol.points(3 * n_steps, 1 + run * config.n_paths + sl.path_lo, sl.n_paths)
+                              for run in runs])
+        obs = [None] * len(variants)
         if sl.n_paths > 0:
-            obs = cuda_backend.exact_batch(params, spec.spot, times, flags, sl.path_lo, sl.path_hi,
-                                           key_run, u)
-            obs_u = obs_d = obs_rp = obs_rm = obs
-            run_ = lambda prm: cuda_backend.exact_batch(prm, spec.spot, times, flags,  # noqa: E731
-                                                       sl.path_lo, sl.path_hi, key_run, u)
-            if want_greeks:
-                obs_u, obs_d = run_(p_up), run_(p_dn)
-                if spec.is_asian:
-                    obs_rp, obs_rm = run_(p_rp), run_(p_rm)
-            q = _per_path(spec, params, obs, obs_u, obs_d, obs_rp, obs_rm, bumps, want_greeks)
-            for i, (lo, hi) in enumerate(jobs):
-                blk = q[lo - sl.path_lo:hi - sl.path_lo]
-                partials[i, 0::2] = blk.sum(axis=0)          # numpy pairwise, engine.py:110
-                partials[i, 1::2] = (blk * blk).sum(axis=0)
-        if world > 1:
-            partials = _gather_rows(partials, config.n_paths, group)
-        for c in range(14):
-            out[run, c] = math.fsum(partials[:, c])           # engine.py:116
+            obs = [cuda_backend.exact_runs(v, spec.spot, times, flags, sl.path_lo, sl.path_hi,
+                                           key_runs, u) for v in variants]
+        for b, run in enumerate(runs):
+            partials = np.zeros((len(jobs), 14))
+            if sl.n_paths > 0:
+                o = [x[b] for x in obs]
+                base = o[0]
+                obs_u, obs_d = (o[1], o[2]) if want_greeks else (base, base)
+                obs_rp, obs_rm = (o[3], o[4]) if want_greeks and spec.is_asian else (base, base)
+                q = _per_path(spec, params, base, obs_u, obs_d, obs_rp, obs_rm, bumps, want_greeks)
+                for i, (lo, hi) in enumerate(jobs):
+                    blk = q[lo - sl.path_lo:hi - sl.path_lo]
+                    partials[i, 0::2] = blk.sum(axis=0)          # numpy pairwise, engine.py:110
+                    partials[i, 1::2] = (blk * blk).sum(axis=0)
+            if world > 1:
+                partials = _gather_rows(partials, config.n_paths, group)
+            for c in range(14):
+                out[run, c] = math.fsum(partials[:, c])           # engine.py:116
     return out
 
 

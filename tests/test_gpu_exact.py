@@ -68,3 +68,21 @@ def test_exact_scrambled_sobol_unbiased_and_tighter(params, euro_call):
     assert len(set(rq.per_run_values)) == 30            # runs are distinct randomisations
     assert abs(rq.estimate - ref) <= 4 * rq.std_error, (rq.estimate, ref, rq.std_error)
     assert rq.std_error / ps.std_error < 0.5
+
+
+def test_exact_runs_equal_per_run_batches(params):
+    """hmc_exact_runs_f64 (all runs in one launch) reproduces one
+    exact_batch call per run exactly, with and without supplied uniforms."""
+    import oracle
+    times, flags = np.array([0.0, 0.25, 0.5]), np.array([1, 1])
+    keys = [oracle.derive_key(oracle.root_key(77), r) for r in range(3)]
+    many = cuda_backend.exact_runs(params, 100.0, times, flags, 10, 1010, keys, None)
+    for r, k in enumerate(keys):
+        one = cuda_backend.exact_batch(params, 100.0, times, flags, 10, 1010, k, None)
+        np.testing.assert_array_equal(many[r], one)
+    rng = np.random.default_rng(3)
+    u = rng.random((3, 500, 6))
+    many = cuda_backend.exact_runs(params, 100.0, times, flags, 0, 500, keys, u)
+    for r, k in enumerate(keys):
+        np.testing.assert_array_equal(many[r], cuda_backend.exact_batch(params, 100.0, times, flags, 0, 500,
+                                                                        k, u[r]))
