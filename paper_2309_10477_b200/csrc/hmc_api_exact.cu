@@ -49,13 +49,8 @@ int hmc_exact_runs_f64(const hmc_model* model, double s0, const double* step_tim
     int dev = 0, sms = 148;
     HMC_CK(cudaGetDevice(&dev));
     HMC_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    long long blocks = (rows + hmc::kExactThreads - 1) / hmc::kExactThreads;
-    // grid-stride kernel: one resident wave is enough, and the node cache
-    // (kExactCacheNodes doubles per thread) is sized by the grid
-    int per_sm = 0;
-    HMC_CK(hmc::exact_occupancy(&per_sm));
-    const long long max_blocks = (long long)sms * (per_sm > 0 ? per_sm : 4);
-    const int grid = (int)(blocks < max_blocks ? blocks : max_blocks);
+    int grid = 0, variant = 4;
+    HMC_CK(hmc::exact_plan(rows, sms, &grid, &variant));
     const size_t threads = (size_t)grid * hmc::kExactThreads;
     cudaStream_t st;
     HMC_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
@@ -91,7 +86,7 @@ int hmc_exact_runs_f64(const hmc_model* model, double s0, const double* step_tim
         e.out = d_o;
         e.scratch = d_s;
         e.err_flag = d_err;
-        if (ce == cudaSuccess) ce = hmc::launch_exact(e, grid, st);
+        if (ce == cudaSuccess) ce = hmc::launch_exact(e, grid, variant, st);
         if (ce == cudaSuccess) ce = cudaMemcpyAsync(out, d_o, ob, cudaMemcpyDeviceToHost, st);
         if (ce == cudaSuccess) ce = cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, st);
         if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);

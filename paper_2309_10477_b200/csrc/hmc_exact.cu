@@ -320,10 +320,13 @@ __device__ double sample_iv(double kappa, double theta, double sigma, double dof
 
 }  // namespace
 
-#ifndef HMC_EXACT_MINB
-#define HMC_EXACT_MINB 1
-#endif
-__global__ void __launch_bounds__(kExactThreads, HMC_EXACT_MINB) exact_batch_kernel(const ExactArgs e) {
+// Two register budgets (tools/exact_prof.py, European, one step):
+// MINB = 3 blocks/SM (158 regs) is fastest for deep grid-stride loops
+// (2^20 paths: 30.0 ms vs 35.0 ms at 4 blocks / 128 regs, 33.5 ms at 2 blocks
+// / 184 regs; 5-8 blocks spill, 38-43 ms), MINB = 4 for jobs of a few waves
+// (2^17 paths: 2.35 ms vs 2.88 ms) -- exact_plan picks per launch.
+template <int MINB>
+__global__ void __launch_bounds__(kExactThreads, MINB) exact_batch_kernel(const ExactArgs e) {
     const long long n = e.path_hi - e.path_lo;
     const long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long stride = (long long)gridDim.x * blockDim.x;
@@ -389,12 +392,27 @@ __global__ void __launch_bounds__(kExactThreads, HMC_EXACT_MINB) exact_batch_ker
     }
 }
 
-cudaError_t exact_occupancy(int* blocks_per_sm) {
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, exact_batch_kernel, kExactThreads, 0);
+cudaError_t exact_plan(long long rows, int sms, int* grid, int* variant) {
+    int occ_wide = 0, occ_deep = 0;
+    cudaError_t err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_wide, exact_batch_kernel<4>,
+                                                                    kExactThreads, 0);
+    if (err == cudaSuccess)
+        err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_deep, exact_batch_kernel<3>, kExactThreads, 0);
+    if (err != cudaSuccess) return err;
+    const long long wave = (long long)sms * (occ_wide > 0 ? occ_wide : 4) * kExactThreads;
+    *variant = rows > 4 * wave ? 3 : 4;  // deep loops: fewer, fatter threads
+    const long long per_sm = *variant == 3 ? (occ_deep > 0 ? occ_deep : 3) : (occ_wide > 0 ? occ_wide : 4);
+    const long long blocks = (rows + kExactThreads - 1) / kExactThreads;
+    const long long max_blocks = (long long)sms * per_sm;  // grid-stride: one resident wave
+    *grid = (int)(blocks < max_blocks ? blocks : max_blocks);
+    return cudaSuccess;
 }
 
-cudaError_t launch_exact(const ExactArgs& e, int grid, cudaStream_t s) {
-    exact_batch_kernel<<<grid, kExactThreads, 0, s>>>(e);
+cudaError_t launch_exact(const ExactArgs& e, int grid, int variant, cudaStream_t s) {
+    if (variant == 3)
+        exact_batch_kernel<3><<<grid, kExactThreads, 0, s>>>(e);
+    else
+        exact_batch_kernel<4><<<grid, kExactThreads, 0, s>>>(e);
     return cudaGetLastError();
 }
 

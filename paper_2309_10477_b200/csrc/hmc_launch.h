@@ -82,8 +82,10 @@ struct ExactArgs {
     int* err_flag;           // max reference error code seen
 };
 
-cudaError_t launch_exact(const ExactArgs& e, int grid, cudaStream_t s);
-cudaError_t exact_occupancy(int* blocks_per_sm);
+// grid (one resident wave, grid-stride) and register variant for `rows`
+// (run, path) pairs; the node cache is sized by grid * kExactThreads
+cudaError_t exact_plan(long long rows, int sms, int* grid, int* variant);
+cudaError_t launch_exact(const ExactArgs& e, int grid, int variant, cudaStream_t s);
 
 // fp32 production kernel (hmc_fast.cu): tiles[run][tile][HMC_NW]
 cudaError_t launch_fast_greeks(const KernelArgs& a, double* d_tiles, long long n_tiles,
