@@ -134,7 +134,9 @@ def execute(params: HestonParams, spec: OptionSpec, config: SimConfig, want_gree
 def _gather_rows(local: np.ndarray, n_paths: int, group) -> np.ndarray:
     import torch
     import torch.distributed as dist
-    dev = torch.device("cuda", torch.cuda.current_device())
+    # NCCL exchanges device tensors; a gloo group (CPU tests) host tensors
+    dev = (torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl"
+           else torch.device("cpu"))
     world = dist.get_world_size(group)
     counts = []
     for r in range(world):
