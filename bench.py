@@ -282,6 +282,10 @@ def run_b200(args) -> None:
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     distributed = "LOCAL_RANK" in os.environ  # launched by torch.distributed.run
+    if args.gpus != world and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch N>1 with "
+              f"torch.distributed.run (one process per GPU) -- reporting n_gpus={world}",
+              file=sys.stderr)
     if distributed:
         dist.init_process_group("nccl", device_id=dev)
     p, spec, cfg = workload()
