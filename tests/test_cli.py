@@ -26,6 +26,15 @@ class TestParsing:
         assert man.spec.strike == man.spec.spot == 100.0 and man.spec.maturity == 1.0
         assert man.config.scheme == "exact" and man.config.precision == "fp32"  # reference default
 
+    def test_sobol_bridge_flag_and_file(self, tmp_path):
+        _, man, _ = parse_config(["greeks", "--scheme", "milstein", "--sampler", "sobol",
+                                  "--sobol-highdim-ack", "--sobol-bridge", "8"])
+        assert man.config.sobol_bridge == 8
+        f = tmp_path / "c.cfg"
+        f.write_text("scheme = milstein\nsampler = sobol\nsobol_highdim_ack = yes\nsobol_bridge = 4\n")
+        _, man, _ = parse_config(["greeks", "--config", str(f)])
+        assert man.config.sobol_bridge == 4
+
     def test_asian_dates(self):
         _, man, _ = parse_config(["price", "--product", "asian", "--averaging-times",
                                   "0.25,0.5,0.75,1"])
@@ -116,6 +125,14 @@ class TestOutputs:
         row = json.loads(out.strip().splitlines()[0])
         assert code == 0 and row["quantity"] == "price" and row["precision"] == "fp64"
         assert row["mean"] > 0
+
+    def test_bridge_flags(self, capsys):
+        code, out, _ = run(capsys, ["greeks", "--format", "jsonl", "--scheme", "milstein", "--sampler",
+                                    "sobol", "--sobol-highdim-ack", "--sobol-scramble", "--sobol-bridge",
+                                    "16", "--paths", "4096", "--steps", "64", "--runs", "4"])
+        row = json.loads(out.strip().splitlines()[0])
+        assert code == 0 and row["sobol_bridge"] == 16 and row["quantity"] == "price"
+        assert abs(row["mean"] - 6.8) < 0.2
 
     def test_surface_csv(self, capsys):
         code, out, _ = run(capsys, ["surface", "--strikes", "90:111:10", "--maturities", "0.5,1",
