@@ -97,6 +97,9 @@ void build_bridge(int S, int n_sim, double dt, Prepared& P) {
 
 int check_model(const hmc_model* m) {
     if (!m) return fail(HMC_E_INVALID, "model is NULL");
+    if (!std::isfinite(m->kappa) || !std::isfinite(m->theta) || !std::isfinite(m->sigma) ||
+        !std::isfinite(m->rho) || !std::isfinite(m->r) || !std::isfinite(m->v0))
+        return fail(HMC_E_INVALID, "model parameters must be finite");
     if (!(m->kappa > 0.0) || !(m->theta > 0.0) || !(m->sigma > 0.0))
         return fail(HMC_E_INVALID, "kappa, theta and sigma must be > 0");
     if (!(m->rho >= -1.0 && m->rho <= 1.0)) return fail(HMC_E_INVALID, "rho must lie in [-1, 1]");
@@ -158,8 +161,9 @@ int prepare(const hmc_model* m, const hmc_product* pr, const hmc_sim* sim, Prepa
     int rc = check_model(m);
     if (rc) return rc;
     if (!pr || !sim) return fail(HMC_E_INVALID, "product/sim is NULL");
-    if (!(pr->strike > 0.0) || !(pr->maturity > 0.0) || !(pr->spot > 0.0))
-        return fail(HMC_E_INVALID, "strike, maturity and spot must be > 0");
+    if (!(pr->strike > 0.0) || !(pr->maturity > 0.0) || !(pr->spot > 0.0) || !std::isfinite(pr->strike) ||
+        !std::isfinite(pr->maturity) || !std::isfinite(pr->spot))
+        return fail(HMC_E_INVALID, "strike, maturity and spot must be finite and > 0");
     if (pr->style != HMC_STYLE_EUROPEAN && pr->style != HMC_STYLE_ASIAN)
         return fail(HMC_E_INVALID, "unknown option style");
     if (pr->right != HMC_CALL && pr->right != HMC_PUT) return fail(HMC_E_INVALID, "unknown option right");
@@ -185,6 +189,8 @@ int prepare(const hmc_model* m, const hmc_product* pr, const hmc_sim* sim, Prepa
     if (pr->style == HMC_STYLE_EUROPEAN && (pr->n_avg != 1 || pr->avg_idx[0] != sim->n_steps))
         return fail(HMC_E_INVALID, "european products fix once, at n_steps");
     if (sim->want_greeks) {
+        if (!std::isfinite(sim->v0_up) || !std::isfinite(sim->h_r))
+            return fail(HMC_E_INVALID, "bump sizes must be finite");
         if (!(sim->h_spot > 0.0 && sim->h_spot < pr->spot)) return fail(HMC_E_INVALID, "need 0 < h_spot < spot");
         if (!(sim->v0_up > sim->v0_dn && sim->v0_dn >= 0.0)) return fail(HMC_E_INVALID, "need v0_up > v0_dn >= 0");
         if (!(sim->h_r > 0.0)) return fail(HMC_E_INVALID, "need h_r > 0");
@@ -578,7 +584,8 @@ int hmc_discretised_batch_f64(const hmc_model* model, double s0, double T, int32
                               int64_t n_avg, double* out, int32_t device) {
     int rc = check_model(model);
     if (rc) return rc;
-    if (n_steps < 1 || !(T > 0.0) || !(s0 > 0.0)) return fail(HMC_E_INVALID, "need n_steps >= 1, T > 0, s0 > 0");
+    if (n_steps < 1 || !(T > 0.0) || !(s0 > 0.0) || !std::isfinite(T) || !std::isfinite(s0))
+        return fail(HMC_E_INVALID, "need n_steps >= 1, finite T > 0 and s0 > 0");
     if (path_hi < path_lo) return fail(HMC_E_INVALID, "path_hi < path_lo");
     if (!avg_idx || n_avg < 1) return fail(HMC_E_INVALID, "avg_idx must hold >= 1 index");
     for (int64_t i = 0; i < n_avg; ++i)

@@ -3,6 +3,7 @@
 // (hmc_sobol_init_directions).
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -19,10 +20,11 @@ int hmc_exact_runs_f64(const hmc_model* model, double s0, const double* step_tim
                        int32_t device) {
     int rc = check_model(model);
     if (rc) return rc;
-    if (!(s0 > 0.0) || n_steps < 1 || !step_times || !avg_flags)
-        return fail(HMC_E_INVALID, "need s0 > 0, n_steps >= 1, step_times and avg_flags");
+    if (!(s0 > 0.0) || !std::isfinite(s0) || n_steps < 1 || !step_times || !avg_flags)
+        return fail(HMC_E_INVALID, "need finite s0 > 0, n_steps >= 1, step_times and avg_flags");
     for (int k = 0; k < n_steps; ++k)
-        if (!(step_times[k + 1] > step_times[k])) return fail(HMC_E_INVALID, "step_times must increase");
+        if (!(step_times[k + 1] > step_times[k]) || !std::isfinite(step_times[k + 1]))
+            return fail(HMC_E_INVALID, "step_times must be finite and increase");
     if (path_hi < path_lo) return fail(HMC_E_INVALID, "path_hi < path_lo");
     if (n_runs < 1 || !key_runs) return fail(HMC_E_INVALID, "need n_runs >= 1 and key_runs");
     const long long n = path_hi - path_lo;

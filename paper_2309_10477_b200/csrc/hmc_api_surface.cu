@@ -25,11 +25,13 @@ struct SurfPrepared {
 
 int check_surface_spec(const hmc_surface_spec* sp, const hmc_sim* sim) {
     if (!sp || !sim) return fail(HMC_E_INVALID, "surface spec / sim is NULL");
-    if (!(sp->spot > 0.0) || !(sp->dt > 0.0)) return fail(HMC_E_INVALID, "need spot > 0 and dt > 0");
+    if (!(sp->spot > 0.0) || !(sp->dt > 0.0) || !std::isfinite(sp->spot) || !std::isfinite(sp->dt))
+        return fail(HMC_E_INVALID, "need finite spot > 0 and dt > 0");
     if (!sp->strikes || sp->n_strikes < 1 || sp->n_strikes > HMC_SURF_MAX_STRIKES)
         return fail(HMC_E_INVALID, "need 1..HMC_SURF_MAX_STRIKES strikes");
     for (int j = 0; j < sp->n_strikes; ++j)
-        if (!(sp->strikes[j] > 0.0) || (j > 0 && !(sp->strikes[j] > sp->strikes[j - 1])))
+        if (!(sp->strikes[j] > 0.0) || !std::isfinite(sp->strikes[j]) ||
+            (j > 0 && !(sp->strikes[j] > sp->strikes[j - 1])))
             return fail(HMC_E_INVALID, "strikes must be positive and strictly increasing");
     if (!sp->mat_idx || sp->n_mats < 1 || sp->n_mats > HMC_SURF_MAX_MATS)
         return fail(HMC_E_INVALID, "need 1..HMC_SURF_MAX_MATS maturities");

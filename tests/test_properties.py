@@ -63,3 +63,26 @@ def test_bridge_is_brownian_motion(S, n):
     t = np.arange(1, n + 1) * dt
     C = bridge.covariance_matrix(S, n, dt)
     assert np.max(np.abs(C - np.minimum.outer(t, t))) <= 1e-14 * max(1.0, n * dt)
+
+
+BAD = st.sampled_from([float("nan"), float("inf"), -float("inf")])
+
+
+@settings(max_examples=60, deadline=None)
+@given(st.sampled_from(["kappa", "theta", "sigma", "rho", "r", "v0", "strike", "maturity", "spot",
+                        "h_r", "v0_up"]), BAD)
+def test_c_abi_rejects_non_finite_inputs(field, bad):
+    """Every floating-point input of a pricing call is validated on the host:
+    NaN / inf never reach a kernel (HMC_E_INVALID, no device work)."""
+    import ctypes
+    m = _lib.Model(2.0, 0.04, 0.3, -0.7, 0.03, 0.04)
+    avg = np.array([64], dtype=np.int64)
+    pr = _lib.Product(0, 0, 100.0, 1.0, 100.0, avg.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), 1)
+    sim = _lib.Sim(scheme=2, sampler=0, precision=0, want_greeks=1, n_steps=64, n_runs=1, n_paths=4096,
+                   path_lo=0, path_hi=4096, seed=1, h_spot=0.5, v0_up=0.0404, v0_dn=0.0396, h_r=1e-4)
+    for obj in (m, pr, sim):
+        if hasattr(obj, field) and field in dict(obj._fields_):
+            setattr(obj, field, bad)
+    buf = ctypes.create_string_buffer(64)
+    rc = _lib.lib().hmc_greeks_chunks(ctypes.byref(m), ctypes.byref(pr), ctypes.byref(sim), buf, buf, None)
+    assert rc == _lib.HMC_E_INVALID
