@@ -239,11 +239,17 @@ int hmc_exact_batch_f64(const hmc_model* model, double s0, const double* step_ti
  * calls exact_batch once per run and 4096-path job, engine.py:93-116):
  * run r uses key_runs[r] (derive_key(root_key(seed), r)); uniforms: HOST
  * [n_runs][path_hi-path_lo][3*n_steps] or NULL; out: HOST
- * [n_runs][path_hi-path_lo][3].  Per-path values equal hmc_exact_batch_f64's. */
+ * [n_runs][path_hi-path_lo][3].  Per-path values equal hmc_exact_batch_f64's.
+ * sobol_v (HOST [30][3*n_steps], hmc_sobol_init_directions layout) or NULL:
+ * with uniforms == NULL the Sobol points are generated on the device --
+ * run r, path p uses point 1 + r*sobol_n_paths + p (engine.py:100), or with
+ * sobol_scramble points 1..N under per-(run, dimension) digital shifts;
+ * identical to passing the same points as uniforms. */
 int hmc_exact_runs_f64(const hmc_model* model, double s0, const double* step_times,
                        int32_t n_steps, const int64_t* avg_flags, int64_t path_lo,
                        int64_t path_hi, const uint64_t* key_runs, int32_t n_runs,
-                       const double* uniforms, double* out, int32_t device);
+                       const double* uniforms, const uint32_t* sobol_v, int32_t sobol_scramble,
+                       int64_t sobol_n_paths, double* out, int32_t device);
 
 /* Joe-Kuo direction numbers as used by scipy.stats.qmc.Sobol(scramble=False)
  * (30 bits): poly[dim], vinit[dim][18] from scipy's

@@ -115,7 +115,8 @@ def _declare(L: ctypes.CDLL) -> None:
         "hmc_exact_batch_f64": (ctypes.c_int, [pM, dbl, pd, i32, ctypes.POINTER(i64), i64, i64, u64,
                                                pd, pd, i32]),
         "hmc_exact_runs_f64": (ctypes.c_int, [pM, dbl, pd, i32, ctypes.POINTER(i64), i64, i64,
-                                              ctypes.POINTER(u64), i32, pd, pd, i32]),
+                                              ctypes.POINTER(u64), i32, pd,
+                                              ctypes.POINTER(ctypes.c_uint32), i32, i64, pd, i32]),
         "hmc_root_key": (u64, [u64]),
         "hmc_derive_key": (u64, [u64, u64]),
     }

@@ -16,8 +16,9 @@ extern "C" {
 
 int hmc_exact_runs_f64(const hmc_model* model, double s0, const double* step_times,
                        int32_t n_steps, const int64_t* avg_flags, int64_t path_lo, int64_t path_hi,
-                       const uint64_t* key_runs, int32_t n_runs, const double* uniforms, double* out,
-                       int32_t device) {
+                       const uint64_t* key_runs, int32_t n_runs, const double* uniforms,
+                       const uint32_t* sobol_v, int32_t sobol_scramble, int64_t sobol_n_paths,
+                       double* out, int32_t device) {
     int rc = check_model(model);
     if (rc) return rc;
     if (!(s0 > 0.0) || !std::isfinite(s0) || n_steps < 1 || !step_times || !avg_flags)
@@ -27,6 +28,12 @@ int hmc_exact_runs_f64(const hmc_model* model, double s0, const double* step_tim
             return fail(HMC_E_INVALID, "step_times must be finite and increase");
     if (path_hi < path_lo) return fail(HMC_E_INVALID, "path_hi < path_lo");
     if (n_runs < 1 || !key_runs) return fail(HMC_E_INVALID, "need n_runs >= 1 and key_runs");
+    if (sobol_v && uniforms) return fail(HMC_E_INVALID, "pass uniforms or sobol_v, not both");
+    if (sobol_v) {
+        const double blocks = sobol_scramble ? 1.0 : (double)n_runs;
+        if (sobol_n_paths < path_hi || 1.0 + blocks * (double)sobol_n_paths > 1073741824.0)
+            return fail(HMC_E_INVALID, "sobol index range exceeds 2^30 points (or n_paths < path_hi)");
+    }
     const long long n = path_hi - path_lo;
     if (n == 0) return HMC_OK;
     const long long rows = n * n_runs;
@@ -61,8 +68,9 @@ int hmc_exact_runs_f64(const hmc_model* model, double s0, const double* step_tim
     const size_t ob = (size_t)rows * 3 * sizeof(double);
     const size_t sb = (size_t)hmc::kExactCacheNodes * threads * sizeof(double);
     const size_t kb = (size_t)n_runs * sizeof(uint64_t);
+    const size_t vb = sobol_v ? (size_t)30 * 3 * n_steps * sizeof(uint32_t) : 0;
     const size_t total = align_up(tb) + align_up(fb) + align_up(ub) + align_up(ob) + align_up(sb) +
-                         align_up(kb) + 256;
+                         align_up(kb) + align_up(vb) + 256;
     char* buf = nullptr;
     int h_err = 0;
     cudaError_t ce = cudaMallocAsync((void**)&buf, total, st);
@@ -74,12 +82,17 @@ int hmc_exact_runs_f64(const hmc_model* model, double s0, const double* step_tim
         double* d_o = (double*)(buf + off); off += align_up(ob);
         double* d_s = (double*)(buf + off); off += align_up(sb);
         unsigned long long* d_k = (unsigned long long*)(buf + off); off += align_up(kb);
+        uint32_t* d_v = sobol_v ? (uint32_t*)(buf + off) : nullptr; off += align_up(vb);
         int* d_err = (int*)(buf + off);
         std::vector<long long> flags(avg_flags, avg_flags + n_steps);
         ce = cudaMemcpyAsync(d_t, step_times, tb, cudaMemcpyHostToDevice, st);
         if (ce == cudaSuccess) ce = cudaMemcpyAsync(d_f, flags.data(), fb, cudaMemcpyHostToDevice, st);
         if (ce == cudaSuccess && uniforms) ce = cudaMemcpyAsync(d_u, uniforms, ub, cudaMemcpyHostToDevice, st);
         if (ce == cudaSuccess) ce = cudaMemcpyAsync(d_k, key_runs, kb, cudaMemcpyHostToDevice, st);
+        if (ce == cudaSuccess && sobol_v) ce = cudaMemcpyAsync(d_v, sobol_v, vb, cudaMemcpyHostToDevice, st);
+        e.sobol_v = d_v;
+        e.sobol_scramble = sobol_scramble ? 1 : 0;
+        e.sobol_n_paths = sobol_n_paths;
         if (ce == cudaSuccess) ce = cudaMemsetAsync(d_err, 0, sizeof(int), st);
         e.key_runs = d_k;
         e.times = d_t;
@@ -111,7 +124,7 @@ int hmc_exact_batch_f64(const hmc_model* model, double s0, const double* step_ti
                         int32_t n_steps, const int64_t* avg_flags, int64_t path_lo, int64_t path_hi,
                         uint64_t key_run, const double* uniforms, double* out, int32_t device) {
     return hmc_exact_runs_f64(model, s0, step_times, n_steps, avg_flags, path_lo, path_hi, &key_run, 1,
-                              uniforms, out, device);
+                              uniforms, nullptr, 0, 0, out, device);
 }
 
 // Bratley-Fox / Joe-Kuo recurrence on the m-values, then the 2^(bits-1-b)

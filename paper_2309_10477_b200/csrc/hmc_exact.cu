@@ -344,6 +344,13 @@ __global__ void __launch_bounds__(kExactThreads, MINB) exact_batch_kernel(const 
         const unsigned long long gamma_root = derive(key_path, 1ULL);
         double ln_s = log(e.s0), v = e.v0, price_sum = 0.0, tw_sum = 0.0;
         const double* urow = e.uniforms ? e.uniforms + (size_t)i * 3 * e.n_steps : nullptr;
+        // on-device Sobol (engine.py:97-101): point 1 + run N + path, or points
+        // 1..N under per-(run, dimension) digital shifts (randomised QMC)
+        uint32_t gray = 0;
+        if (e.sobol_v) {
+            const uint32_t idx = (uint32_t)(1 + (e.sobol_scramble ? 0LL : run * e.sobol_n_paths) + e.path_lo + p);
+            gray = idx ^ (idx >> 1);
+        }
         for (int k = 0; k < e.n_steps; ++k) {
             const double dt = e.times[k + 1] - e.times[k];
             double u1, u2, u3;
@@ -351,6 +358,20 @@ __global__ void __launch_bounds__(kExactThreads, MINB) exact_batch_kernel(const 
                 u1 = urow[3 * k];
                 u2 = urow[3 * k + 1];
                 u3 = urow[3 * k + 2];
+            } else if (e.sobol_v) {
+                double uu[3];
+                for (int j = 0; j < 3; ++j) {
+                    uint32_t x = sobol_coord(gray, e.sobol_v, 3 * e.n_steps, 3 * k + j);
+                    double half = 0.0;
+                    if (e.sobol_scramble) {
+                        x ^= sobol_shift(e.key_runs[run], 3 * k + j);
+                        half = 0.5;
+                    }
+                    uu[j] = ((double)x + half) * (1.0 / 1073741824.0);
+                }
+                u1 = uu[0];
+                u2 = uu[1];
+                u3 = uu[2];
             } else {
                 u1 = uniform_at(main_key, (unsigned long long)(3 * k));
                 u2 = uniform_at(main_key, (unsigned long long)(3 * k + 1));

@@ -77,6 +77,9 @@ struct ExactArgs {
     const unsigned long long* key_runs;  // [n_runs] per-run stream keys (device)
     int n_runs;
     const double* uniforms;  // [n_runs][n][3 n_steps] or null
+    const uint32_t* sobol_v; // [30][3 n_steps] Sobol direction numbers (device) or null
+    int sobol_scramble;      // digital shifts per (run, dimension)
+    long long sobol_n_paths; // N of the run blocks 1 + run N + path
     double* out;             // [n_runs][n][3]
     double* scratch;         // [kExactCacheNodes][grid threads]
     int* err_flag;           // max reference error code seen

@@ -96,10 +96,13 @@ def exact_batch(params, s0: float, step_times, avg_flags, path_lo: int, path_hi:
 
 
 def exact_runs(params, s0: float, step_times, avg_flags, path_lo: int, path_hi: int, key_runs,
-               uniforms) -> np.ndarray:
+               uniforms, sobol=None) -> np.ndarray:
     """``exact_batch`` for several runs in one launch: run r uses
     ``key_runs[r]``; ``uniforms`` is None or (n_runs, n, 3*n_steps).
-    Returns (n_runs, n, 3) -- each run's rows equal ``exact_batch``'s."""
+    ``sobol = (directions [30, 3*n_steps], scramble, n_paths)`` generates the
+    Sobol points on the device instead (same points as the host's
+    ``sobol.points``).  Returns (n_runs, n, 3) -- each run's rows equal
+    ``exact_batch``'s."""
     times = np.ascontiguousarray(step_times, dtype=np.float64)
     flags = np.ascontiguousarray(avg_flags, dtype=np.int64)
     n_steps = times.size - 1
@@ -113,12 +116,20 @@ def exact_runs(params, s0: float, step_times, avg_flags, path_lo: int, path_hi: 
         u = np.ascontiguousarray(uniforms, dtype=np.float64)
         if u.shape != (keys.size, n, 3 * n_steps):
             raise ValueError("uniforms must be (n_runs, path_hi - path_lo, 3 * n_steps)")
+    v, scramble, n_total = None, 0, 0
+    if sobol is not None:
+        v = np.ascontiguousarray(sobol[0], dtype=np.uint32)
+        if v.shape != (30, 3 * n_steps):
+            raise ValueError("sobol directions must be (30, 3 * n_steps)")
+        scramble, n_total = int(bool(sobol[1])), int(sobol[2])
     m = _lib.Model(params.kappa, params.theta, params.sigma, params.rho, params.r, params.v0)
     pd = ctypes.POINTER(ctypes.c_double)
     rc = _lib.lib().hmc_exact_runs_f64(
         ctypes.byref(m), float(s0), times.ctypes.data_as(pd), n_steps,
         flags.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), int(path_lo), int(path_hi),
         keys.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), keys.size,
-        None if u is None else u.ctypes.data_as(pd), out.ctypes.data_as(pd), _device())
+        None if u is None else u.ctypes.data_as(pd),
+        None if v is None else v.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), scramble, n_total,
+        out.ctypes.data_as(pd), _device())
     _lib.check(rc)
     return out

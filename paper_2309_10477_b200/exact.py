@@ -95,23 +95,20 @@ def execute(params: HestonParams, spec: OptionSpec, config: SimConfig, want_gree
         variants += [p_up, p_dn] + ([p_rp, p_rm] if spec.is_asian else [])
     # runs go to the GPU in batches (one launch per model variant and batch);
     # a batch is bounded so the host buffers stay ~<= 256 MB
-    per_run_bytes = max(sl.n_paths, 1) * 8 * (3 * len(variants) + (3 * n_steps if config.sampler == "sobol" else 0))
+    per_run_bytes = max(sl.n_paths, 1) * 8 * 3 * len(variants)
     batch = max(1, min(config.n_runs, (256 << 20) // per_run_bytes))
+    # Sobol points (engine.py:97-101) are generated on the device from the
+    # direction numbers -- the same points as sobol.points on the host
+    sob = None
+    if config.sampler == "sobol":
+        sob = (sobol.directions(3 * n_steps), bool(config.sobol_scramble), config.n_paths)
     for r0 in range(0, config.n_runs, batch):
         runs = range(r0, min(config.n_runs, r0 + batch))
         key_runs = [_lib.lib().hmc_derive_key(key_root, run) for run in runs]
-        u = None
-        if config.sampler == "sobol" and sl.n_paths > 0:  # engine.py:97-101
-            if config.sobol_scramble:      # randomised QMC: points 1..N, per-run shifts
-                u = np.stack([sobol.points(3 * n_steps, 1 + sl.path_lo, sl.n_paths, key_run=k)
-                              for k in key_runs])
-            else:
-                u = np.stack([sobol.points(3 * n_steps, 1 + run * config.n_paths + sl.path_lo, sl.n_paths)
-                              for run in runs])
         obs = [None] * len(variants)
         if sl.n_paths > 0:
             obs = [cuda_backend.exact_runs(v, spec.spot, times, flags, sl.path_lo, sl.path_hi,
-                                           key_runs, u) for v in variants]
+                                           key_runs, None, sobol=sob) for v in variants]
         for b, run in enumerate(runs):
             partials = np.zeros((len(jobs), 14))
             if sl.n_paths > 0:

@@ -86,3 +86,24 @@ def test_exact_runs_equal_per_run_batches(params):
     for r, k in enumerate(keys):
         np.testing.assert_array_equal(many[r], cuda_backend.exact_batch(params, 100.0, times, flags, 0, 500,
                                                                         k, u[r]))
+
+
+@pytest.mark.parametrize("scramble", [False, True])
+def test_exact_device_sobol_equals_host_points(params, scramble):
+    """Sobol points generated inside the exact kernel equal the host's
+    sobol.points (reference block 1 + run N + path, or points 1..N under
+    per-run digital shifts): per-path outputs identical."""
+    import oracle
+    from paper_2309_10477_b200 import sobol
+    times, flags = np.array([0.0, 0.25, 0.5, 0.75, 1.0]), np.array([1, 1, 1, 1])
+    N, lo, hi = 3000, 1000, 2500
+    keys = [oracle.derive_key(oracle.root_key(5), r) for r in range(2)]
+    dev = cuda_backend.exact_runs(params, 100.0, times, flags, lo, hi, keys, None,
+                                  sobol=(sobol.directions(12), scramble, N))
+    for r, k in enumerate(keys):
+        if scramble:
+            u = sobol.points(12, 1 + lo, hi - lo, key_run=k)
+        else:
+            u = sobol.points(12, 1 + r * N + lo, hi - lo)
+        host = cuda_backend.exact_batch(params, 100.0, times, flags, lo, hi, k, u)
+        np.testing.assert_array_equal(dev[r], host)

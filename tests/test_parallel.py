@@ -92,7 +92,7 @@ def test_gather_world2_matches_single(n):
     np.testing.assert_array_equal(_seq_reduce(torch.tensor(got[1])), _seq_reduce(torch.tensor(single)))
 
 
-def _fake_exact_runs(params, s0, times, flags, path_lo, path_hi, key_runs, uniforms):
+def _fake_exact_runs(params, s0, times, flags, path_lo, path_hi, key_runs, uniforms, sobol=None):
     """CPU stand-in for cuda_backend.exact_runs: deterministic per-path
     observables of (key_run, global path index, model)."""
     idx = np.arange(path_lo, path_hi, dtype=np.float64)
