@@ -27,6 +27,32 @@ int fail(int code, const std::string& msg) {
     return code;
 }
 
+namespace {
+struct ThreadStreams {
+    std::vector<cudaStream_t> by_device;
+    ~ThreadStreams() {
+        for (cudaStream_t st : by_device)
+            if (st) cudaStreamDestroy(st);
+    }
+};
+thread_local ThreadStreams t_streams;
+}  // namespace
+
+cudaError_t call_stream(int device, cudaStream_t* out) {
+    if (device < 0 || device >= 1024) return cudaErrorInvalidDevice;
+    if ((size_t)device >= t_streams.by_device.size()) t_streams.by_device.resize((size_t)device + 1, nullptr);
+    cudaStream_t& st = t_streams.by_device[device];
+    if (!st) {
+        cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+        if (e != cudaSuccess) {
+            st = nullptr;
+            return e;
+        }
+    }
+    *out = st;
+    return cudaSuccess;
+}
+
 // The one-call entry points allocate their device buffers from the
 // device's default stream-ordered pool.  With the pool's default release
 // threshold (0) every synchronize hands the memory back to the driver and
@@ -461,7 +487,7 @@ int hmc_greeks(const hmc_model* model, const hmc_product* product, const hmc_sim
     HMC_CK(cudaSetDevice(device));
     HMC_CK(keep_pool_memory(device));
     cudaStream_t s;
-    HMC_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    HMC_CK(call_stream(device, &s));
     const size_t work = (size_t)hmc_workspace_bytes(&sim);
     const size_t chunk_bytes = (size_t)sim.n_runs * P.n_chunks * HMC_NW * sizeof(double);
     const size_t out_bytes = (size_t)sim.n_runs * HMC_NW * sizeof(double);
@@ -479,7 +505,6 @@ int hmc_greeks(const hmc_model* model, const hmc_product* product, const hmc_sim
         cudaFreeAsync(buf, s);
     }
     cudaError_t e2 = cudaStreamSynchronize(s);
-    cudaStreamDestroy(s);
     if (rc) return rc;
     HMC_CK(e);
     HMC_CK(e2);
@@ -614,7 +639,7 @@ int hmc_discretised_batch_f64(const hmc_model* model, double s0, double T, int32
     HMC_CK(cudaSetDevice(device));
     HMC_CK(keep_pool_memory(device));
     cudaStream_t s;
-    HMC_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    HMC_CK(call_stream(device, &s));
     const size_t ub = uniforms ? (size_t)n * 2 * n_steps * sizeof(double) : 0;
     const size_t ob = (size_t)n * 3 * sizeof(double);
     const size_t tb = P.st64.size() * sizeof(StepD);
@@ -633,7 +658,6 @@ int hmc_discretised_batch_f64(const hmc_model* model, double s0, double T, int32
         cudaFreeAsync(buf, s);
     }
     cudaError_t e2 = cudaStreamSynchronize(s);
-    cudaStreamDestroy(s);
     HMC_CK(e);
     HMC_CK(e2);
     return HMC_OK;

@@ -62,7 +62,7 @@ int hmc_exact_runs_f64(const hmc_model* model, double s0, const double* step_tim
     HMC_CK(hmc::exact_plan(rows, sms, &grid, &variant));
     const size_t threads = (size_t)grid * hmc::kExactThreads;
     cudaStream_t st;
-    HMC_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    HMC_CK(call_stream(device, &st));
     const size_t tb = ((size_t)n_steps + 1) * sizeof(double), fb = (size_t)n_steps * sizeof(long long);
     const size_t ub = uniforms ? (size_t)rows * 3 * n_steps * sizeof(double) : 0;
     const size_t ob = (size_t)rows * 3 * sizeof(double);
@@ -108,7 +108,6 @@ int hmc_exact_runs_f64(const hmc_model* model, double s0, const double* step_tim
         cudaFreeAsync(buf, st);
     }
     cudaError_t ce2 = cudaStreamSynchronize(st);
-    cudaStreamDestroy(st);
     HMC_CK(ce);
     HMC_CK(ce2);
     switch (h_err) {  // _core.pyx:508-520

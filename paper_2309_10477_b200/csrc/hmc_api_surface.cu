@@ -230,7 +230,7 @@ int hmc_surface(const hmc_model* model, const hmc_surface_spec* spec, const hmc_
     HMC_CK(cudaSetDevice(device));
     HMC_CK(keep_pool_memory(device));
     cudaStream_t st;
-    HMC_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    HMC_CK(call_stream(device, &st));
     const size_t acc_bytes = (size_t)hmc_surface_acc_words(spec, sim.n_runs) * sizeof(int64_t);
     const size_t work = (size_t)hmc_surface_workspace_bytes(spec, &sim);
     std::vector<int64_t> h_acc(acc_bytes / sizeof(int64_t));
@@ -247,7 +247,6 @@ int hmc_surface(const hmc_model* model, const hmc_surface_spec* spec, const hmc_
         cudaFreeAsync(buf, st);
     }
     cudaError_t e2 = cudaStreamSynchronize(st);
-    cudaStreamDestroy(st);
     if (rc) return rc;
     HMC_CK(e);
     HMC_CK(e2);

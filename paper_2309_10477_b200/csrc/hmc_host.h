@@ -48,6 +48,11 @@ struct DeviceGuard {
     DeviceGuard& operator=(const DeviceGuard&) = delete;
 };
 
+// The one-call entry points run on a per-thread, per-device non-blocking
+// stream created on first use and destroyed at thread exit (creating and
+// destroying a stream per call costs more than a small job's kernel).
+cudaError_t call_stream(int device, cudaStream_t* out);
+
 // keep freed blocks in the device's default stream-ordered pool (hmc_api.cu)
 cudaError_t keep_pool_memory(int dev);
 
