@@ -52,7 +52,15 @@ def workload():
     return p, spec, cfg
 
 
-def secondary_workloads(reps: int = 3) -> dict:
+# canonical MUFU ops per path-step of each secondary workload (the MUFU
+# roofline): European full Greeks 4 (Box-Muller) + 3
+# sqrt(v); Sobol 2 lg2 (quantiles) + 3 sqrt + 3 ex2; surface = the Asian
+# step (10).  The Sobol drivers are issue-bound, not MUFU-bound, so their
+# fraction is a lower bound on how busy the chip is.
+SECONDARY_MUFU = {"c2": 7, "c4": 8, "c5": 10}
+
+
+def secondary_workloads(reps: int = 3, sm_mhz: float = 1965.0) -> dict:
     """The other BASELINE configs on one GPU through the public API (CUDA
     events around each call; host overhead included)."""
     import numpy as np
@@ -99,6 +107,10 @@ def secondary_workloads(reps: int = 3) -> dict:
             ts.append(e0.elapsed_time(e1))
         ms = sorted(ts)[len(ts) // 2]
         out[name] = {"ms": ms, "path_steps_per_s": path_steps / (ms / 1e3)}
+        mufu = SECONDARY_MUFU.get(name[:2])
+        if mufu:
+            peak = N_SM * 16 * sm_mhz * 1e6 / mufu
+            out[name].update(mufu_per_path_step=mufu, mufu_roofline_frac=path_steps / (ms / 1e3) / peak)
     return out
 
 
@@ -394,7 +406,7 @@ def run_b200(args) -> None:
         if world == 1 and not args.no_cpu:
             line["cpu_baseline"] = cpu_baseline_block()
         if world == 1 and not args.no_e2e:
-            line["secondary"] = secondary_workloads()
+            line["secondary"] = secondary_workloads(sm_mhz=f_mhz)
             if not args.no_cpu:
                 line["cpu_baseline_exact"] = cpu_exact_block()
         print(json.dumps(line))
