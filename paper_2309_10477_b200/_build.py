@@ -56,7 +56,7 @@ def build(verbose: bool = False, force: bool = False, defines: dict | None = Non
     dflags = [f"-D{k}={v}" for k, v in (defines or {}).items()]
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(ROOT, "include", "hmc.h"))
-    objs = []
+    objs, cmds = [], []
     for unit, extra in UNITS.items():
         src = os.path.join(CSRC, unit)
         obj = os.path.join(objdir, unit.replace(".cu", ".o"))
@@ -66,7 +66,12 @@ def build(verbose: bool = False, force: bool = False, defines: dict | None = Non
             if verbose:
                 cmd += ["-Xptxas", "-v"]
                 print(" ".join(cmd), flush=True)
-            subprocess.run(cmd, check=True)
+            cmds.append(cmd)
+    # translation units compile independently: run them concurrently
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max(1, min(len(cmds), os.cpu_count() or 1))) as pool:
+        for fut in [pool.submit(subprocess.run, c, check=True) for c in cmds]:
+            fut.result()
     if force or _stale(lib, objs):
         cmd = [nvcc(), *ARCH, "-shared", "-o", lib, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
         if verbose:
