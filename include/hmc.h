@@ -263,6 +263,12 @@ int hmc_sobol_init_directions(const int64_t* poly, const int64_t* vinit,
  * tests of the exact device code path.  Synchronous. */
 int hmc_philox_check(const uint32_t* ctr, int32_t n, uint32_t* out, int32_t device);
 
+/* The fp32 kernels' Sobol quantile z = Phi^-1(u) on n HOST 30-bit
+ * coordinates x[n] (u = x 2^-30, or (x + 1/2) 2^-30 when scrambled) ->
+ * out[n]; known-answer tests of the device code path.  Synchronous. */
+int hmc_sobol_quantile_check(const uint32_t* x, int32_t n, int32_t scrambled, float* out,
+                             int32_t device);
+
 /* Key derivation of the reference RNG (rng.py:46-52), for hosts that
  * build key_run for hmc_discretised_batch_f64. */
 uint64_t hmc_root_key(uint64_t seed);

@@ -365,6 +365,16 @@ __global__ void philox_kat_kernel(const uint4* __restrict__ ctr, uint4* __restri
     }
 }
 
+// the production kernels' Sobol quantile on given 30-bit coordinates
+__global__ void sobol_quantile_kernel(const uint32_t* __restrict__ x, int n, float half,
+                                      float* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        const float ht = half * 9.31322574615478515625e-10f;
+        out[i] = kSqrt2f * sobol_normal_u(x[i], 2.0f * ht, ht);
+    }
+}
+
 cudaError_t launch_chunks_to_runs(const double* d_chunks, long long n_chunks, int n_runs,
                                   double* d_out, cudaStream_t s) {
     chunks_to_runs_kernel<<<(unsigned)n_runs, kRunThreads, 0, s>>>(d_chunks, n_chunks, d_out);
@@ -678,6 +688,29 @@ int hmc_philox_check(const uint32_t* ctr, int32_t n, uint32_t* out, int32_t devi
     if (e == cudaSuccess) e = cudaMemcpy(out, d_o, (size_t)n * sizeof(uint4), cudaMemcpyDeviceToHost);
     cudaFree(d_c);
     cudaFree(d_o);
+    HMC_CK(e);
+    return HMC_OK;
+}
+
+int hmc_sobol_quantile_check(const uint32_t* x, int32_t n, int32_t scrambled, float* out,
+                             int32_t device) {
+    if (!x || !out || n < 1) return fail(HMC_E_INVALID, "bad quantile check arguments");
+    for (int32_t i = 0; i < n; ++i)
+        if (x[i] >= (1u << 30) || (!scrambled && x[i] == 0))
+            return fail(HMC_E_INVALID, "coordinates are 30-bit, and >= 1 unless scrambled");
+    const DeviceGuard keep_device;
+    HMC_CK(cudaSetDevice(device));
+    char* buf = nullptr;
+    const size_t xb = align_up((size_t)n * sizeof(uint32_t)), ob = align_up((size_t)n * sizeof(float));
+    HMC_CK(cudaMalloc((void**)&buf, xb + ob));
+    cudaError_t e = cudaMemcpy(buf, x, (size_t)n * sizeof(uint32_t), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        hmc::sobol_quantile_kernel<<<(n + 127) / 128, 128>>>((const uint32_t*)buf, n, scrambled ? 0.5f : 0.0f,
+                                                            (float*)(buf + xb));
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(out, buf + xb, (size_t)n * sizeof(float), cudaMemcpyDeviceToHost);
+    cudaFree(buf);
     HMC_CK(e);
     return HMC_OK;
 }

@@ -11,6 +11,7 @@
 
 #include "hmc_device.cuh"
 #include "hmc_launch.h"
+#include "hmc_path32.cuh"
 
 namespace hmc_host {
 
@@ -74,6 +75,7 @@ struct Prepared {
 };
 
 int check_model(const hmc_model* m);
+
 // validate one single-product job and build its arguments and tables
 int prepare(const hmc_model* m, const hmc_product* pr, const hmc_sim* sim, Prepared& P);
 // workspace bytes of the Brownian-bridge tables

@@ -193,10 +193,11 @@ __device__ __forceinline__ void box_muller(uint32_t xr, uint32_t xa, const Kerne
 // (callers fold sqrt(2) into their constants); hx = half 2^-29 and
 // ht = half 2^-30 are loop invariants of the caller.
 __device__ __forceinline__ float sobol_normal_u(uint32_t x, float hx, float ht) {
-    const uint32_t t = min(x, (1u << 30) - x);              // min(u, 1-u) 2^30 (- half)
+    const bool hi = x >= (1u << 29);
+    const uint32_t t = hi ? (1u << 30) - x : x;              // min(u, 1-u) 2^30 (-+ half)
     const int m = (int)(2u * x) - (1 << 30);                // (2u - 1) 2^30 - 2 half
     const float xs = fmaf((float)m, 9.31322574615478515625e-10f, hx);
-    const float tf = fmaf((float)t, 9.31322574615478515625e-10f, ht);
+    const float tf = fmaf((float)t, 9.31322574615478515625e-10f, hi ? -ht : ht);
     // w = -ln(4 tf (1 - tf)) = -ln2 (lg2(tf (1 - tf)) + 2)
     float w = fmaf(lg2a(tf * (1.0f - tf)), -0.69314718055994530942f, -1.38629436111989061883f);
     float p;
@@ -228,9 +229,21 @@ __device__ __forceinline__ float sobol_normal_u(uint32_t x, float hx, float ht) 
         q = fmaf(q, wt, 1.00167406f);
         q = fmaf(q, wt, 2.83297682f);
         p = w >= 5.0f ? q : p;
+        // extreme cells (t = min(u, 1 - u) < ~3e-8): Giles' single-precision
+        // erfinv is built for float inputs (w <= ~16); use Acklam's lower-tail
+        // rational (the reference's ndtri, _core.pyx:75-109) on t instead
+        if (__any_sync(0xffffffffu, w >= 16.0f)) {
+            const float qa = sqrta(-1.38629436111989061883f * lg2a(tf));   // sqrt(-2 ln t)
+            const float num = fmaf(fmaf(fmaf(fmaf(fmaf(-7.784894002430293e-03f, qa, -3.223964580411365e-01f), qa,
+                                                 -2.400758277161838e+00f), qa, -2.549732539343734e+00f), qa,
+                                       4.374664141464968e+00f), qa, 2.938163982698783e+00f);
+            const float den = fmaf(fmaf(fmaf(fmaf(7.784695709041462e-03f, qa, 3.224671290700398e-01f), qa,
+                                            2.445134137142996e+00f), qa, 3.754408661907416e+00f), qa, 1.0f);
+            const float z = __fdividef(num, den) * 0.70710678118654752440f;   // lower tail: z < 0
+            if (w >= 16.0f) return hi ? -z : z;
+        }
     }
 #else
-    float p;
     if (w < 5.0f) {
         w = w - 2.5f;
         p = 2.81022636e-08f;
@@ -259,6 +272,7 @@ __device__ __forceinline__ float sobol_normal_u(uint32_t x, float hx, float ht) 
 }
 
 constexpr float kSqrt2f = 1.41421356237309504880f;
+
 
 struct PathState32 {
     float v0, L0, A0;  // base trajectory
