@@ -263,6 +263,13 @@ int hmc_sobol_init_directions(const int64_t* poly, const int64_t* vinit,
  * tests of the exact device code path.  Synchronous. */
 int hmc_philox_check(const uint32_t* ctr, int32_t n, uint32_t* out, int32_t device);
 
+/* The fp32 kernels' Box-Muller on n HOST Philox blocks words[n][4] ->
+ * out[n][6]: the three standard-normal pairs (z1, z2) the production step
+ * loop draws from one block (radius from the top 23 bits of w0/w1/w2,
+ * angles from w3 and the low bits; hmc_path32.cuh tri_unpack).  Known-answer
+ * and distribution tests of the device code path.  Synchronous. */
+int hmc_box_muller_check(const uint32_t* words, int32_t n, float* out, int32_t device);
+
 /* The fp32 kernels' Sobol quantile z = Phi^-1(u) on n HOST 30-bit
  * coordinates x[n] (u = x 2^-30, or (x + 1/2) 2^-30 when scrambled) ->
  * out[n]; known-answer tests of the device code path.  Synchronous. */

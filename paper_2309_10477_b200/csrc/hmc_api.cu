@@ -365,6 +365,25 @@ __global__ void philox_kat_kernel(const uint4* __restrict__ ctr, uint4* __restri
     }
 }
 
+// the production kernels' Box-Muller on given Philox blocks: three (z1, z2)
+// standard-normal pairs per block (KernelArgs set so the folded constants
+// reduce to sqrt(-2 ln u1) (cos, sin))
+__global__ void box_muller_kat_kernel(const uint4* __restrict__ w, int n, KernelArgs a,
+                                      float* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        const uint4 x = w[i];
+        float fr[3], fa[3];
+        tri_unpack(x, fr, fa);
+        for (int k = 0; k < 3; ++k) {
+            float z1, z2;
+            box_muller_f(fr[k], fa[k], x.x << (31 - k), a, z1, z2);
+            out[6 * i + 2 * k] = z1;
+            out[6 * i + 2 * k + 1] = z2;
+        }
+    }
+}
+
 // the production kernels' Sobol quantile on given 30-bit coordinates
 __global__ void sobol_quantile_kernel(const uint32_t* __restrict__ x, int n, float half,
                                       float* __restrict__ out) {
@@ -688,6 +707,28 @@ int hmc_philox_check(const uint32_t* ctr, int32_t n, uint32_t* out, int32_t devi
     if (e == cudaSuccess) e = cudaMemcpy(out, d_o, (size_t)n * sizeof(uint4), cudaMemcpyDeviceToHost);
     cudaFree(d_c);
     cudaFree(d_o);
+    HMC_CK(e);
+    return HMC_OK;
+}
+
+int hmc_box_muller_check(const uint32_t* words, int32_t n, float* out, int32_t device) {
+    if (!words || !out || n < 1) return fail(HMC_E_INVALID, "bad box-muller check arguments");
+    const DeviceGuard keep_device;
+    HMC_CK(cudaSetDevice(device));
+    KernelArgs a{};
+    a.f_bm2 = (float)(-2.0 * std::log(2.0));  // R = sqrt(-2 ln u1)
+    a.f_cA = 0.0f;                            // second output = R sin
+    a.f_cB = 1.0f;
+    char* buf = nullptr;
+    const size_t wb = align_up((size_t)n * sizeof(uint4)), ob = (size_t)n * 6 * sizeof(float);
+    HMC_CK(cudaMalloc((void**)&buf, wb + ob));
+    cudaError_t e = cudaMemcpy(buf, words, (size_t)n * sizeof(uint4), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        hmc::box_muller_kat_kernel<<<(n + 127) / 128, 128>>>((const uint4*)buf, n, a, (float*)(buf + wb));
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(out, buf + wb, ob, cudaMemcpyDeviceToHost);
+    cudaFree(buf);
     HMC_CK(e);
     return HMC_OK;
 }

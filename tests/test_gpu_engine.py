@@ -374,3 +374,80 @@ class TestSobolQuantile:
         # monotone in u (ties allowed at fp32 resolution)
         order = np.argsort(u, kind="stable")
         assert np.all(np.diff(out[order]) >= -1e-6)
+
+
+class TestBoxMuller:
+    """The production normals: hmc_box_muller_check runs the kernels'
+    tri_unpack + box_muller_f on given Philox blocks."""
+
+    @staticmethod
+    def _device(words):
+        from paper_2309_10477_b200 import _lib
+        w = np.ascontiguousarray(words, dtype=np.uint32)
+        out = np.empty((w.shape[0], 6), dtype=np.float32)
+        _lib.check(_lib.lib().hmc_box_muller_check(w.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)),
+                                                   w.shape[0], out.ctypes.data_as(ctypes.POINTER(ctypes.c_float)),
+                                                   0))
+        return out.astype(np.float64)
+
+    @staticmethod
+    def _restated(w):
+        """The documented bit layout (hmc_path32.cuh tri_unpack) in fp64."""
+        w = w.astype(np.uint64)
+        m32 = np.uint64(0xFFFFFFFF)
+        f = lambda bits: (bits.astype(np.uint32).view(np.float32)).astype(np.float64)  # noqa: E731
+        one = np.uint64(0x3F800000)
+        fr = [f((w[:, k] >> np.uint64(9)) + one) for k in range(3)]
+        fa = [f(((w[:, 3] >> np.uint64(9)) & np.uint64(0x007FFFF0)) | one),
+              f((((w[:, 3] << np.uint64(10)) & m32) & np.uint64(0x007FFC00))
+                | (((w[:, 0] << np.uint64(1)) & m32) & np.uint64(0x000003F0)) | one),
+              f((((w[:, 1] << np.uint64(14)) & m32) & np.uint64(0x007FC000))
+                | (((w[:, 2] << np.uint64(5)) & m32) & np.uint64(0x00003FE0)) | one)]
+        out = np.empty((w.shape[0], 6))
+        for k in range(3):
+            r = np.sqrt(-2.0 * np.log(2.0 - fr[k]))
+            th = 2.0 * np.pi * fa[k] - 3.0 * np.pi
+            out[:, 2 * k], out[:, 2 * k + 1] = r * np.cos(th), r * np.sin(th)
+        return out
+
+    def test_bit_layout_known_answers(self):
+        rng = np.random.default_rng(5)
+        w = rng.integers(0, 2**32, size=(200_000, 4), dtype=np.uint64).astype(np.uint32)
+        w[:4] = [[0, 0, 0, 0], [0xFFFFFFFF] * 4, [0x80000000, 1, 0x7FFFFFFF, 0xFFFF0000],
+                 [0x00000200, 0x00000200, 0x00000200, 0x00001000]]
+        got, ref = self._device(w), self._restated(w)
+        err = np.abs(got - ref) / np.maximum(1.0, np.abs(ref))
+        # MUFU.LG2's absolute error near 1 dominates the radius when u1 -> 1
+        # (R = sqrt(-2 ln u1) < 0.01, probability ~5e-5 per draw): absolute
+        # error there up to ~2e-4 in z; a few fp32 ulps everywhere else
+        r2 = ref[:, 0::2] ** 2 + ref[:, 1::2] ** 2
+        small = np.repeat(r2 < 1e-4, 2, axis=1)
+        assert err[~small].max() < 5e-6, err[~small].max()
+        assert np.abs(got - ref)[small].max(initial=0.0) < 3e-4
+
+    def test_production_stream_is_standard_normal(self):
+        """Philox4x32-10 blocks on production counters (step triple, path,
+        key_run) through the device transform: 6e6 normals with N(0, 1)
+        moments, no correlation within a block, KS against the normal CDF."""
+        import oracle
+        from scipy import stats
+        from paper_2309_10477_b200 import _lib
+        n = 1_000_000
+        key = oracle.derive_key(oracle.root_key(42), 0)
+        ctr = np.zeros((n, 4), dtype=np.uint32)
+        ctr[:, 0] = np.arange(n) % 84
+        ctr[:, 1] = np.arange(n) // 84
+        ctr[:, 2], ctr[:, 3] = key & 0xFFFFFFFF, key >> 32
+        words = np.empty_like(ctr)
+        _lib.check(_lib.lib().hmc_philox_check(ctr.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), n,
+                                               words.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), 0))
+        z = self._device(words)
+        flat = z.ravel()
+        m = flat.size
+        assert abs(flat.mean()) < 5 / math.sqrt(m)
+        assert abs(flat.var() - 1.0) < 5 * math.sqrt(2.0 / m)
+        assert abs(stats.skew(flat)) < 5 * math.sqrt(6.0 / m)
+        assert abs(stats.kurtosis(flat)) < 5 * math.sqrt(24.0 / m)
+        c = np.corrcoef(z.T)
+        assert np.max(np.abs(c - np.eye(6))) < 5 / math.sqrt(n)
+        assert stats.kstest(flat[:2_000_000], "norm").pvalue > 1e-4
