@@ -263,6 +263,16 @@ int hmc_sobol_init_directions(const int64_t* poly, const int64_t* vinit,
  * tests of the exact device code path.  Synchronous. */
 int hmc_philox_check(const uint32_t* ctr, int32_t n, uint32_t* out, int32_t device);
 
+/* The fp32 production step arithmetic (state, Milstein/Euler update,
+ * fixings, CRN trajectories, per-path estimators -- the code of
+ * hmc_greeks_chunks' kernel) driven by GIVEN standard normals: HOST
+ * normals[n][n_sim][2] = (z1, z2), z2 independent of z1 (correlated inside
+ * as the kernels do), n_sim = the last fixing index; out: HOST
+ * [n][HMC_NQ] per-path quantities.  Known-answer parity of the fp32 path
+ * against the fp64 oracle on identical shocks.  Synchronous. */
+int hmc_fp32_paths_check(const hmc_model* model, const hmc_product* product, const hmc_sim* sim,
+                         const float* normals, int64_t n, double* out, int32_t device);
+
 /* The fp32 kernels' Box-Muller on n HOST Philox blocks words[n][4] ->
  * out[n][6]: the three standard-normal pairs (z1, z2) the production step
  * loop draws from one block (radius from the top 23 bits of w0/w1/w2,

@@ -42,7 +42,7 @@ EXPORTS = (
     "hmc_chunks_in_slice", "hmc_workspace_bytes", "hmc_greeks_chunks",
     "hmc_reduce_chunks", "hmc_greeks", "hmc_greeks_multi", "hmc_discretised_batch_f64",
     "hmc_sobol_init_directions", "hmc_root_key", "hmc_derive_key", "hmc_philox_check",
-    "hmc_sobol_quantile_check", "hmc_box_muller_check",
+    "hmc_sobol_quantile_check", "hmc_box_muller_check", "hmc_fp32_paths_check",
     "hmc_surface_acc_words", "hmc_surface_workspace_bytes", "hmc_surface_partials",
     "hmc_surface_finalize", "hmc_surface", "hmc_exact_batch_f64", "hmc_exact_runs_f64",
 )
@@ -105,6 +105,7 @@ def _declare(L: ctypes.CDLL) -> None:
                                                      pd, ctypes.POINTER(i64), i64, pd, i32]),
         "hmc_sobol_init_directions": (ctypes.c_int, [ctypes.POINTER(i64), ctypes.POINTER(i64),
                                                      i32, ctypes.POINTER(ctypes.c_uint32)]),
+        "hmc_fp32_paths_check": (ctypes.c_int, [pM, pP, pS, ctypes.POINTER(ctypes.c_float), i64, pd, i32]),
         "hmc_box_muller_check": (ctypes.c_int, [ctypes.POINTER(ctypes.c_uint32), i32,
                                                 ctypes.POINTER(ctypes.c_float), i32]),
         "hmc_sobol_quantile_check": (ctypes.c_int, [ctypes.POINTER(ctypes.c_uint32), i32, i32,

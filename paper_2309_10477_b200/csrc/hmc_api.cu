@@ -174,6 +174,7 @@ void fill_fp32_constants(KernelArgs& a) {
     a.f_disc = (float)a.disc;
     a.f_disc_up = (float)a.disc_up;
     a.f_disc_dn = (float)a.disc_dn;
+    a.f_ddisc = (float)(a.disc_up - a.disc_dn);
     a.f_inv_s0 = (float)(1.0 / a.s0);
     a.f_up_ratio = (float)((a.s0 + a.h_spot) / a.s0);
     a.f_dn_ratio = (float)((a.s0 - a.h_spot) / a.s0);
@@ -707,6 +708,42 @@ int hmc_philox_check(const uint32_t* ctr, int32_t n, uint32_t* out, int32_t devi
     if (e == cudaSuccess) e = cudaMemcpy(out, d_o, (size_t)n * sizeof(uint4), cudaMemcpyDeviceToHost);
     cudaFree(d_c);
     cudaFree(d_o);
+    HMC_CK(e);
+    return HMC_OK;
+}
+
+int hmc_fp32_paths_check(const hmc_model* model, const hmc_product* product, const hmc_sim* sim_in,
+                         const float* normals, int64_t n, double* out, int32_t device) {
+    if (!sim_in || !normals || !out || n < 1) return fail(HMC_E_INVALID, "bad paths check arguments");
+    hmc_sim sim = *sim_in;
+    sim.want_greeks = 1;
+    sim.sampler = HMC_SAMPLER_PSEUDO;
+    sim.precision = HMC_PREC_FP32;
+    sim.sobol_bridge = 0;
+    sim.n_runs = 1;
+    sim.n_paths = n;
+    sim.path_lo = 0;
+    sim.path_hi = n;
+    Prepared P;
+    int rc = prepare(model, product, &sim, P);
+    if (rc) return rc;
+    const DeviceGuard keep_device;
+    HMC_CK(cudaSetDevice(device));
+    const size_t zb = align_up((size_t)n * P.a.n_sim * sizeof(float2));
+    const size_t ob = align_up((size_t)n * HMC_NQ * sizeof(double));
+    const size_t t64 = align_up(P.st64.size() * sizeof(StepD)), t32 = P.st32.size() * sizeof(float4);
+    char* buf = nullptr;
+    HMC_CK(cudaMalloc((void**)&buf, zb + ob + t64 + t32));
+    cudaError_t e = cudaMemcpy(buf, normals, (size_t)n * P.a.n_sim * sizeof(float2), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(buf + zb + ob, P.st64.data(), P.st64.size() * sizeof(StepD), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(buf + zb + ob + t64, P.st32.data(), t32, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        P.a.steps64 = (const StepD*)(buf + zb + ob);
+        P.a.steps32 = (const float4*)(buf + zb + ob + t64);
+        e = hmc::launch_given_normals(P.a, (const float2*)buf, n, (double*)(buf + zb), 0);
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(out, buf + zb, (size_t)n * HMC_NQ * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(buf);
     HMC_CK(e);
     return HMC_OK;
 }

@@ -103,7 +103,7 @@ struct KernelArgs {
     // fp32 epilogue constants (no double->float conversions or divisions on
     // the device: F2F and MUFU.RCP share the MIO queue with the path MUFUs)
     float f_v0, f_vu, f_vd;
-    float f_K, f_T, f_disc, f_disc_up, f_disc_dn;
+    float f_K, f_T, f_disc, f_disc_up, f_disc_dn, f_ddisc;  // f_ddisc = disc_up - disc_dn (fp64)
     float f_inv_s0, f_up_ratio, f_dn_ratio;   // 1/S0, (S0 +- h)/S0
     float f_inv_2h, f_inv_dv, f_inv_2hr;      // 1/(2 h_S), 1/(v0u - v0d), 1/(2 h_r)
     float f_inv_navg;
@@ -264,8 +264,17 @@ __device__ __forceinline__ void greeks_epilogue(const KernelArgs& a, T A, T tw, 
 
 // fp32 twin of greeks_epilogue: same estimators, host-precomputed
 // reciprocals instead of divisions
+// fp32 per-path estimators.  dp, dm are the r-bumped underlyings' offsets
+// Rp - A, Rm - A (accumulated directly, no cancellation).  The FD Greeks of
+// a call are evaluated in cancellation-free form: where both bumped
+// underlyings are in the money the finite difference is linear in the path,
+//   delta_fd = d A / S0                     ((A(1+e) - A(1-e)) / 2h = A / S0)
+//   rho_fd   = ((A - K) (d+ - d-) + d+ dp - d- dm) / 2h_r
+// with d+ - d- from the host in fp64 (rounding d+ and d- separately and
+// subtracting cost ~3e-5 relative bias in rho_fd); on the band where only
+// the up-bumped one is, it is the single term d+ (Rp - K) / 2h.
 __device__ __forceinline__ void greeks_epilogue_f32(const KernelArgs& a, float A, float tw, float Au,
-                                                    float Ad, float Rp, float Rm, double (&q)[kNQ]) {
+                                                    float Ad, float dp, float dm, double (&q)[kNQ]) {
     const float K = a.f_K, disc = a.f_disc;
     auto payoff = [&](float x, float d) -> float {
         return a.is_call ? d * pos_part(x - K) : d * pos_part(K - x);
@@ -279,9 +288,17 @@ __device__ __forceinline__ void greeks_epilogue_f32(const KernelArgs& a, float A
     const float Aup = A * a.f_up_ratio, Adn = A * a.f_dn_ratio;
     const float ind = (float)((Aup > K) ? 1 : 0) - (float)((Adn > K) ? 1 : 0);
     q[HMC_Q_GAMMA] = (double)(ind * dA * a.f_inv_2h);
-    q[HMC_Q_DELTA_FD] = (double)((payoff(Aup, disc) - payoff(Adn, disc)) * a.f_inv_2h);
     q[HMC_Q_VEGA] = (double)((payoff(Au, disc) - payoff(Ad, disc)) * a.f_inv_dv);
-    q[HMC_Q_RHO_FD] = (double)((payoff(Rp, a.f_disc_up) - payoff(Rm, a.f_disc_dn)) * a.f_inv_2hr);
+    const float Rp = A + dp, Rm = A + dm;
+    if (a.is_call) {
+        q[HMC_Q_DELTA_FD] = Adn > K ? (double)dA : (double)(disc * pos_part(Aup - K) * a.f_inv_2h);
+        q[HMC_Q_RHO_FD] =
+            Rm > K ? (double)(fmaf(A - K, a.f_ddisc, fmaf(a.f_disc_up, dp, -a.f_disc_dn * dm)) * a.f_inv_2hr)
+                   : (double)(a.f_disc_up * pos_part(Rp - K) * a.f_inv_2hr);
+    } else {
+        q[HMC_Q_DELTA_FD] = (double)((payoff(Aup, disc) - payoff(Adn, disc)) * a.f_inv_2h);
+        q[HMC_Q_RHO_FD] = (double)((payoff(Rp, a.f_disc_up) - payoff(Rm, a.f_disc_dn)) * a.f_inv_2hr);
+    }
 }
 
 }  // namespace hmc

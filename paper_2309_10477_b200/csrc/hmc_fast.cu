@@ -329,8 +329,8 @@ __global__ void HMC_BOUNDS fast_greeks_kernel(const KernelArgs a,
     const float A = st.A0 * inv_n;
     double q[kNQ];
     if (GREEKS) {
-        greeks_epilogue_f32(a, A, st.T1 * inv_n, st.Au * inv_n, st.Ad * inv_n,
-                            fmaf(st.Dp, inv_n, A), fmaf(st.Dm, inv_n, A), q);
+        greeks_epilogue_f32(a, A, st.T1 * inv_n, st.Au * inv_n, st.Ad * inv_n, st.Dp * inv_n,
+                            st.Dm * inv_n, q);
     } else {
         const float K = a.f_K, disc = a.f_disc;
         q[0] = (double)(a.is_call ? disc * pos_part(A - K) : disc * pos_part(K - A));
@@ -366,6 +366,48 @@ static void launch_greeks_flag(const KernelArgs& a, double* d_tiles, long long n
         launch_sampler<FIX, true>(a, d_tiles, n_tiles, grid, s);
     else
         launch_sampler<FIX, false>(a, d_tiles, n_tiles, grid, s);
+}
+
+// Known-answer path of the production arithmetic: the same state, step,
+// fixing and epilogue code as fast_greeks_kernel, driven by GIVEN standard
+// normals z[path][k] = (z1, z2) (z2 independent of z1; correlated as in
+// the kernels), per-path quantities out[path][HMC_NQ] (no reduction).
+template <int FIX>
+__global__ void __launch_bounds__(kTile) given_normals_kernel(const KernelArgs a, const float2* __restrict__ z,
+                                                              long long n, double* __restrict__ out) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    PathState32 st;
+    st.v0 = a.f_v0;
+    st.vu = a.f_vu;
+    st.vd = a.f_vd;
+    st.L0 = st.Lu = st.Ld = 0.0f;
+    st.A0 = st.Au = st.Ad = 0.0f;
+    st.T1 = st.Dp = st.Dm = 0.0f;
+    const float c1 = a.f_sqdt * a.f_log2e, cs = a.f_sigma * a.f_sqdt;
+    for (int k = 1; k <= a.n_sim; ++k) {
+        const float2 w = z[(size_t)i * a.n_sim + (k - 1)];
+        step<FIX, true>(st, k, c1 * w.x, cs * fmaf(a.f_rho, w.x, a.f_sq1mr2 * w.y), a);
+    }
+    if (FIX == kFixLast) fixing<true>(st, __ldg(a.steps32 + a.n_sim));
+    const float inv_n = a.f_inv_navg;
+    const float A = st.A0 * inv_n;
+    double q[kNQ];
+    greeks_epilogue_f32(a, A, st.T1 * inv_n, st.Au * inv_n, st.Ad * inv_n, st.Dp * inv_n, st.Dm * inv_n,
+                        q);
+#pragma unroll
+    for (int j = 0; j < kNQ; ++j) out[(size_t)i * kNQ + j] = q[j];
+}
+
+cudaError_t launch_given_normals(const KernelArgs& a, const float2* d_z, long long n, double* d_out,
+                                 cudaStream_t s) {
+    const unsigned grid = (unsigned)((n + kTile - 1) / kTile);
+    switch (a.fix_mode) {
+        case kFixLast: given_normals_kernel<kFixLast><<<grid, kTile, 0, s>>>(a, d_z, n, d_out); break;
+        case kFixEvery: given_normals_kernel<kFixEvery><<<grid, kTile, 0, s>>>(a, d_z, n, d_out); break;
+        default: given_normals_kernel<kFixTable><<<grid, kTile, 0, s>>>(a, d_z, n, d_out); break;
+    }
+    return cudaGetLastError();
 }
 
 cudaError_t launch_fast_greeks(const KernelArgs& a, double* d_tiles, long long n_tiles,

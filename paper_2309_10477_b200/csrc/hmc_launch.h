@@ -90,6 +90,10 @@ struct ExactArgs {
 cudaError_t exact_plan(long long rows, int sms, int* grid, int* variant);
 cudaError_t launch_exact(const ExactArgs& e, int grid, int variant, cudaStream_t s);
 
+// the production step arithmetic on given normals (hmc_fast.cu), per path
+cudaError_t launch_given_normals(const KernelArgs& a, const float2* d_z, long long n, double* d_out,
+                                 cudaStream_t s);
+
 // fp32 production kernel (hmc_fast.cu): tiles[run][tile][HMC_NW]
 cudaError_t launch_fast_greeks(const KernelArgs& a, double* d_tiles, long long n_tiles,
                                cudaStream_t s);
