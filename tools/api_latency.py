@@ -1,3 +1,5 @@
+"""Host-side latency of the public API (greeks()) for small and large jobs, with a
+cProfile of the Python layer (dev tool; run on the GPU box)."""
 import os, sys, time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)

@@ -1,3 +1,5 @@
+"""Exact-scheme GPU outputs vs the reference's golden vectors
+(tests/golden/exact_cases.npz) plus a throughput probe (dev tool)."""
 import json, os, sys, time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT); sys.path.insert(0, os.path.join(ROOT, "tests"))

@@ -1,3 +1,5 @@
+"""Device Philox4x32-10 against a host restatement and a price probe on the
+production stream (dev tool)."""
 import ctypes, os, sys
 import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

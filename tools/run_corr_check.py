@@ -1,3 +1,5 @@
+"""Independence of per-run estimates on the production stream: correlation
+between runs derived from one seed (dev tool)."""
 import math, os, sys
 import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

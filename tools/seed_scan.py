@@ -1,3 +1,5 @@
+"""fp32 production estimates over many seeds vs the semi-analytic price:
+z-score distribution (bias check, dev tool)."""
 import math, os, sys
 import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
