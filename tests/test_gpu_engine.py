@@ -309,9 +309,14 @@ class TestSobol:
                   n_steps=n_steps, n_runs=3, seed=17, sobol_scramble=scramble)
         a = greeks(bench_params, spec, SimConfig(**kw))
         b = greeks(bench_params, spec, SimConfig(precision="fp64", **kw))
-        for q in ("price", "delta", "rho"):
-            np.testing.assert_allclose(a[q].per_run_values, b[q].per_run_values, rtol=2e-4, atol=1e-5,
+        # same points: every estimator to fp32 accuracy (FD Greeks included,
+        # via the cancellation-free epilogue); Gamma is an indicator
+        # difference, so one path flipping at a band edge moves it by O(1/N)
+        for q in ("price", "delta", "rho", "vega", "delta_fd", "rho_fd"):
+            np.testing.assert_allclose(a[q].per_run_values, b[q].per_run_values, rtol=3e-5, atol=1e-6,
                                        err_msg=q)
+        np.testing.assert_allclose(a["gamma"].per_run_values, b["gamma"].per_run_values, rtol=5e-3,
+                                   err_msg="gamma")
 
     def test_scrambled_sobol_finite_at_scale(self, bench_params):
         """Shifted coordinates can be exactly 0 (x == shift): the quantile
