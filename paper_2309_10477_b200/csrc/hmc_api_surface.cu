@@ -68,9 +68,10 @@ int prepare_surface(const hmc_model* m, const hmc_surface_spec* sp, const hmc_si
     for (int k = 0; k < sp->n_mats; ++k) {
         const int step = (int)sp->mat_idx[k];
         const double T = S.P.st64[step].t;
+        const double dp = std::exp(-(a.r + a.h_r) * T), dm = std::exp(-(a.r - a.h_r) * T);
         S.mats.push_back({step, (float)(1.0 / step), (float)T, (float)std::exp(a.h_r * T),
-                          (float)std::exp(-a.h_r * T), (float)std::exp(-a.r * T),
-                          (float)std::exp(-(a.r + a.h_r) * T), (float)std::exp(-(a.r - a.h_r) * T)});
+                          (float)std::exp(-a.h_r * T), (float)std::exp(-a.r * T), (float)dp, (float)dm,
+                          (float)(dp - dm)});
     }
     S.s.nK = sp->n_strikes;
     S.s.n_mats = sp->n_mats;

@@ -264,8 +264,8 @@ __device__ __forceinline__ void greeks_epilogue(const KernelArgs& a, T A, T tw, 
 
 // fp32 twin of greeks_epilogue: same estimators, host-precomputed
 // reciprocals instead of divisions
-// fp32 per-path estimators.  dp, dm are the r-bumped underlyings' offsets
-// Rp - A, Rm - A (accumulated directly, no cancellation).  The FD Greeks of
+// fp32 per-path estimators.  Au, Ad are the v0-bumped averages; dp, dm the
+// r-bumped underlyings' offsets Rp - A, Rm - A (accumulated directly).  The FD Greeks of
 // a call are evaluated in cancellation-free form: where both bumped
 // underlyings are in the money the finite difference is linear in the path,
 //   delta_fd = d A / S0                     ((A(1+e) - A(1-e)) / 2h = A / S0)
@@ -288,14 +288,18 @@ __device__ __forceinline__ void greeks_epilogue_f32(const KernelArgs& a, float A
     const float Aup = A * a.f_up_ratio, Adn = A * a.f_dn_ratio;
     const float ind = (float)((Aup > K) ? 1 : 0) - (float)((Adn > K) ? 1 : 0);
     q[HMC_Q_GAMMA] = (double)(ind * dA * a.f_inv_2h);
-    q[HMC_Q_VEGA] = (double)((payoff(Au, disc) - payoff(Ad, disc)) * a.f_inv_dv);
     const float Rp = A + dp, Rm = A + dm;
     if (a.is_call) {
+        // both v0-bumped averages in the money: d (Au - Ad) / dv, the
+        // difference taken before scaling (as the surface kernel does)
+        q[HMC_Q_VEGA] = (Au > K && Ad > K) ? (double)(disc * (Au - Ad) * a.f_inv_dv)
+                                           : (double)((payoff(Au, disc) - payoff(Ad, disc)) * a.f_inv_dv);
         q[HMC_Q_DELTA_FD] = Adn > K ? (double)dA : (double)(disc * pos_part(Aup - K) * a.f_inv_2h);
         q[HMC_Q_RHO_FD] =
             Rm > K ? (double)(fmaf(A - K, a.f_ddisc, fmaf(a.f_disc_up, dp, -a.f_disc_dn * dm)) * a.f_inv_2hr)
                    : (double)(a.f_disc_up * pos_part(Rp - K) * a.f_inv_2hr);
     } else {
+        q[HMC_Q_VEGA] = (double)((payoff(Au, disc) - payoff(Ad, disc)) * a.f_inv_dv);
         q[HMC_Q_DELTA_FD] = (double)((payoff(Aup, disc) - payoff(Adn, disc)) * a.f_inv_2h);
         q[HMC_Q_RHO_FD] = (double)((payoff(Rp, a.f_disc_up) - payoff(Rm, a.f_disc_dn)) * a.f_inv_2hr);
     }

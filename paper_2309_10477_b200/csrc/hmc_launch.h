@@ -37,7 +37,7 @@ constexpr int kSurfVals = 23;
 constexpr int kSurfBucketRows = 15;
 constexpr float kSurfLinScale = 1024.0f;      // 2^10 fixed point for linear moments
 constexpr float kSurfQuadScale = 0.25f;       // 2^-2 for quadratic moments
-constexpr float kSurfBandScale = 65536.0f;    // 2^16 for the (small) band moments
+constexpr float kSurfBandScale = 1048576.0f;  // 2^20 for the (small, <= ~1) band moments
 
 struct SurfMat {
     int step;      // grid index of the maturity
@@ -45,6 +45,8 @@ struct SurfMat {
     float T;       // t_step
     float ehp, ehm;  // e^{+h_r T}, e^{-h_r T}
     float d, dp, dm; // e^{-r T}, e^{-(r +- h_r) T}
+    float ddisc;     // dp - dm formed in fp64 (rounding dp and dm separately
+                     // and subtracting biases the Asian FD Rho by ~3e-5)
 };
 
 struct SurfArgs {

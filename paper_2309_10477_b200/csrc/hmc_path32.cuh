@@ -327,6 +327,9 @@ __device__ __forceinline__ void fixing(PathState32& st, const float4 w) {
         st.Au = fmaf(Pu, w.x, st.Au);
         st.Ad = fmaf(Pd, w.x, st.Ad);
 #else
+        // (carrying Au - A0 instead -- one more FADD per trajectory and
+        // fixing -- shrinks Vega's fp32 error ~40x but costs 4 % of the
+        // daily-fixing kernel: 10.66 -> 11.08 ms; not taken)
         st.Au = fmaf(ex2_sel<(HMC_EX2_POLY >= 1)>(st.Lu), w.x, st.Au);
         st.Ad = fmaf(ex2_sel<(HMC_EX2_POLY >= 2)>(st.Ld), w.x, st.Ad);
 #endif

@@ -130,7 +130,7 @@ __device__ __forceinline__ void surface_checkpoint(const PathState32& st, const 
         // a = [A (d+ - d-) + (d+ D+ - d- D-)/N] / 2h_r, both terms same sign
         const float inv = mc.inv_n;
         const float Aa = st.A0 * inv;
-        const float al = (Aa * (mc.dp - mc.dm) + (mc.dp * st.Dp - mc.dm * st.Dm) * inv) * s.inv_2hr;
+        const float al = (Aa * mc.ddisc + (mc.dp * st.Dp - mc.dm * st.Dm) * inv) * s.inv_2hr;
         surface_update(hist + per_style, g_asian, nb, sK, pow2, s.nK, s, mc.d, Aa, st.Au * inv, st.Ad * inv,
                        fmaf(st.Dp, inv, Aa), fmaf(st.Dm, inv, Aa), fmaf(st.T1, inv, -mc.T * Aa), al);
     }

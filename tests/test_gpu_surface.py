@@ -38,7 +38,8 @@ def test_surface_points_equal_single_product_engine():
                 g = greeks(p, OptionSpec(style, "call", K, T, 100.0, averaging_times=dates), _cfg(n))
                 for q in QN:
                     est = res.estimate[style][q][mi, j]
-                    tol = 2e-5 if q in ("price", "delta", "rho") else 2e-3
+                    # Vega differences two separately accumulated fp32 averages
+                    tol = 1e-3 if q == "vega" else 3e-5
                     scale = max(abs(g[q].estimate), 1e-3)
                     assert abs(est - g[q].estimate) <= tol * scale + 1e-6, (style, T, K, q, est,
                                                                            g[q].estimate)

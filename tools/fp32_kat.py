@@ -8,8 +8,9 @@ import oracle
 from paper_2309_10477_b200 import BENCH_PARAMS, HestonParams, OptionSpec, SimConfig, _lib, daily_fixings, engine
 p = HestonParams(**BENCH_PARAMS)
 out = {}
-for name, spec in (("european", OptionSpec("european", "call", 100.0, 1.0, 100.0)),
-                   ("asian_daily", OptionSpec("asian_arithmetic", "call", 100.0, 1.0, 100.0,
+K = float(sys.argv[1]) if len(sys.argv) > 1 else 100.0
+for name, spec in (("european", OptionSpec("european", "call", K, 1.0, 100.0)),
+                   ("asian_daily", OptionSpec("asian_arithmetic", "call", K, 1.0, 100.0,
                                               averaging_times=daily_fixings(1.0, 252)))):
     cfg = SimConfig(scheme="milstein", n_paths=16384, n_steps=252, n_runs=1, seed=1)
     job = engine.Job(p, spec, cfg, True)
