@@ -18,15 +18,29 @@
  *                                 per-run sums and sums of squares of
  *                                 price / Delta / Rho (+ Gamma, Vega, FD
  *                                 Delta, FD Rho from CRN bumps)
+ *   hmc_greeks_multi           <- the same job dealt over several GPUs from
+ *                                 one process (engine.py:104-116 workers)
+ *   hmc_exact_batch_f64 / hmc_exact_runs_f64
+ *                              <- backend module call exact_batch
+ *                                 (_core.pyx:415-521), per run / all runs
+ *   hmc_surface* (partials, finalize, one-call)
+ *                              <- no reference counterpart: strike x maturity
+ *                                 grids of the engine's estimators (BASELINE
+ *                                 config 5) from one path set
  *   hmc_sobol_init_directions  <- scipy.stats.qmc.Sobol direction numbers
  *                                 used by rng.sobol_points (rng.py:143-152)
  *   hmc_root_key / hmc_derive_key
  *                              <- rng.root_key / rng.derive_key (rng.py:46-52)
+ *   hmc_philox_check / hmc_box_muller_check / hmc_sobol_quantile_check /
+ *   hmc_fp32_paths_check       <- test hooks: the device code paths of the
+ *                                 fp32 kernels on given inputs (known-answer
+ *                                 tests, tests/test_gpu_engine.py)
  *
  * Errors: every function returns 0 on success or a negative HMC_E* code;
  * hmc_last_error() gives a thread-local message for the last failure.
  * Threading: all entry points are re-entrant (no global mutable state apart
- * from the thread-local error string); buffers are caller-owned.
+ * from the thread-local error string, a per-thread stream cache and a
+ * once-per-device pool setting); buffers are caller-owned.
  */
 #ifndef HMC_H_
 #define HMC_H_
