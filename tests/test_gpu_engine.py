@@ -506,16 +506,18 @@ class TestFp32PathsKnownAnswer:
                 3 * ref[:, c].std() / math.sqrt(n) * 0.05, (c, got[:, c].mean(), ref[:, c].mean())
 
 
-@pytest.mark.parametrize("over", [dict(v0=0.0), dict(rho=1.0), dict(rho=-1.0), dict(sigma=2.0, theta=0.01),
-                                  dict(kappa=0.05, sigma=0.9)])
-def test_fp32_paths_known_answer_edge_params(over):
+@pytest.mark.parametrize("over,scheme", [(dict(v0=0.0), "milstein"), (dict(rho=1.0), "milstein"),
+                                         (dict(rho=-1.0), "milstein"), (dict(sigma=2.0, theta=0.01), "milstein"),
+                                         (dict(kappa=0.05, sigma=0.9), "milstein"), ({}, "euler"),
+                                         (dict(sigma=2.0, theta=0.01), "euler")])
+def test_fp32_paths_known_answer_edge_params(over, scheme):
     """Same normals, edge regimes (v0 = 0 one-sided bump, perfect
     correlation, frequent truncation at v = 0, slow mean reversion): the
     fp32 arithmetic stays within fp32 accuracy of the fp64 oracle."""
     from paper_2309_10477_b200 import _lib
     p = HestonParams(**{**BENCH_PARAMS, **over})
     spec = OptionSpec("asian_arithmetic", "call", 100.0, 1.0, 100.0, averaging_times=daily_fixings(1.0, 64))
-    cfg = SimConfig(scheme="milstein", n_paths=8192, n_steps=64, n_runs=1, seed=1)
+    cfg = SimConfig(scheme=scheme, n_paths=8192, n_steps=64, n_runs=1, seed=1)
     job = engine.Job(p, spec, cfg, True)
     n = 8192
     z = np.random.default_rng(23).standard_normal((n, 64, 2)).astype(np.float32)
@@ -526,7 +528,8 @@ def test_fp32_paths_known_answer_edge_params(over):
     zz = np.zeros((n, 128))
     zz[:, 0::2] = z[:, :, 0]
     zz[:, 1::2] = p.rho * z[:, :, 0].astype(np.float64) + math.sqrt(max(1 - p.rho ** 2, 0.0)) * z[:, :, 1]
-    ref = oracle.greeks_paths_z(p, spec, 64, True, zz, job.avg_idx, engine.bump_sizes(p, spec, cfg))
+    ref = oracle.greeks_paths_z(p, spec, 64, scheme == "milstein", zz, job.avg_idx,
+                                engine.bump_sizes(p, spec, cfg))
     assert np.all(np.isfinite(got))
     assert np.max(np.abs(got[:, 0] - ref[:, 0])) < 2e-3
     for c in range(7):
