@@ -17,7 +17,8 @@
 #define HMC_EX2_POLY 0
 #endif
 #ifndef HMC_SOBOL_VOTE
-#define HMC_SOBOL_VOTE 1     // Sobol quantile: warp-voted tail branch (all 32 lanes must be active)
+#define HMC_SOBOL_VOTE 1     // Sobol quantile: warp-voted tail branches (all 32 lanes must be active;
+                             // 0 = the divergent if/else without the extreme-cell branch, experiments only)
 #endif
 #ifndef HMC_SQRT_RSQ
 #define HMC_SQRT_RSQ 0
