@@ -18,7 +18,6 @@ engine computes for ``OptionSpec(strike=K, maturity=T_m)`` with
 from __future__ import annotations
 
 import ctypes
-import math
 import time
 from dataclasses import dataclass, field
 

@@ -11,7 +11,7 @@ import pytest
 from conftest import GOLDEN
 from paper_2309_10477_b200 import (BesselNonConvergence, HestonParams, OptionSpec, SimConfig,
                                    cuda_backend, price)
-from paper_2309_10477_b200.model import BENCH_PARAMS, DEFAULT_PARAMS
+from paper_2309_10477_b200.model import BENCH_PARAMS
 
 pytestmark = pytest.mark.gpu
 

@@ -12,7 +12,7 @@ from scipy.special import ndtr
 
 import oracle
 from paper_2309_10477_b200 import cuda_backend
-from paper_2309_10477_b200.model import DEFAULT_PARAMS, BENCH_PARAMS, HestonParams
+from paper_2309_10477_b200.model import DEFAULT_PARAMS, HestonParams
 
 pytestmark = pytest.mark.gpu
 

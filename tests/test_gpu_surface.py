@@ -3,7 +3,6 @@ the single-product engine's estimate on the same paths; integer histograms
 make any split of the paths bit-identical."""
 
 import ctypes
-import math
 
 import numpy as np
 import pytest

@@ -5,8 +5,6 @@ golden vectors the reference produced (tests/golden/make_golden.py) and, when
 oracle/_ref was built here, the reference kernel itself on fresh inputs.
 """
 
-import math
-import types
 
 import numpy as np
 import pytest

@@ -3,7 +3,6 @@ inverse normal (reference tests/test_rng.py:98-104 style monotonicity and
 symmetry), the key derivation of the C ABI against the oracle, the host
 Sobol points, and the Brownian-bridge construction -- CPU only."""
 
-import math
 
 import numpy as np
 from hypothesis import given, settings
