@@ -60,3 +60,24 @@ def test_greeks_multi_bit_identical(n_paths, n_runs, n_dev):
                                   multi.ctypes.data_as(pd), devs, n_dev))
     assert np.array_equal(one, multi)
     assert np.all(one[:, 0] > 0)
+
+
+def test_integration_md_ctypes_stub_runs():
+    """The plain-ctypes backend stub printed in INTEGRATION.md (what a
+    reference maintainer would paste into hestonmc/backend.py) is executable
+    and returns what cuda_backend.discretised_batch returns."""
+    import re
+    import numpy as np
+    from paper_2309_10477_b200 import cuda_backend
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    blocks = re.findall(r"```python\n(.*?)```", text, re.S)
+    stub = next(b for b in blocks if "hmc_discretised_batch_f64" in b and "argtypes" in b)
+    lib = os.path.join(ROOT, "paper_2309_10477_b200", "libhmc.so")
+    ns = {}
+    exec(compile(stub.replace('"libhmc.so"', repr(lib)), "INTEGRATION.md", "exec"), ns)
+    p = HestonParams(**BENCH_PARAMS)
+    avg = np.array([8, 16, 24, 32])
+    got = ns["discretised_batch"](p, 100.0, 1.0, 32, True, 0, 256, 12345, None, avg)
+    ref = cuda_backend.discretised_batch(p, 100.0, 1.0, 32, True, 0, 256, 12345, None, avg)
+    assert ns["BACKEND_NAME"] == "cuda"
+    np.testing.assert_array_equal(got, ref)
