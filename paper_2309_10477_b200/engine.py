@@ -65,6 +65,22 @@ def bump_sizes(params: HestonParams, spec: OptionSpec, config: SimConfig) -> tup
             config.bump_r)
 
 
+_DIRECTIONS_ON_DEVICE: dict = {}
+
+
+def _device_directions(host: np.ndarray, dev):
+    """Sobol direction numbers on the device, uploaded once per (table,
+    device): the tables are immutable (sobol.directions is cached and
+    read-only), so repeated QMC calls skip the 60 KB upload."""
+    import torch
+    key = (host.shape, dev.index, id(host))
+    hit = _DIRECTIONS_ON_DEVICE.get(key)
+    if hit is None or hit[0] is not host:
+        hit = (host, torch.from_numpy(np.array(host)).to(dev))
+        _DIRECTIONS_ON_DEVICE[key] = hit
+    return hit[1]
+
+
 class Job:
     """ctypes image of one (params, spec, config) request."""
 
@@ -111,7 +127,7 @@ class Job:
         sl = parallel.shard(self.n_paths, rank, world)
         keep = []
         if self.sobol_host is not None:
-            v = torch.from_numpy(np.array(self.sobol_host)).to(dev, non_blocking=False)
+            v = _device_directions(self.sobol_host, dev)
             keep.append(v)
             self.sim.sobol_v = ctypes.cast(ctypes.c_void_p(v.data_ptr()), ctypes.POINTER(ctypes.c_uint32))
             self.sim.sobol_v_on_device = 1
