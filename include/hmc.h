@@ -265,6 +265,22 @@ int hmc_exact_runs_f64(const hmc_model* model, double s0, const double* step_tim
                        const double* uniforms, const uint32_t* sobol_v, int32_t sobol_scramble,
                        int64_t sobol_n_paths, double* out, int32_t device);
 
+/* The exact scheme's engine path (engine._run_sums with scheme="exact",
+ * engine.py:71-116) on the device: for the chunk-aligned slice
+ * [sim->path_lo, sim->path_hi) of every run, the base simulation and (with
+ * sim->want_greeks) the v0 +- and -- for Asians -- r +- re-simulations on
+ * the same streams, the per-path estimators of hmc_greeks (Rho-FD of a
+ * European by exact e^{+-h T} rescaling) and per-chunk partials
+ * d_chunks[run][chunk][HMC_NW] (DEVICE) in the same layout as
+ * hmc_greeks_chunks, so hmc_reduce_chunks and multi-GPU gathers apply
+ * unchanged.  step_times / avg_flags as hmc_exact_batch_f64; sampler pseudo
+ * (reference stream) or sobol (sim->sobol_v, on-device points).  Runs on
+ * `stream`, synchronous on return (numerical failures are reported like
+ * hmc_exact_batch_f64's). */
+int hmc_exact_greeks_chunks(const hmc_model* model, const hmc_product* product, const hmc_sim* sim,
+                            const double* step_times, int32_t n_steps, const int64_t* avg_flags,
+                            double* d_chunks, void* stream);
+
 /* Joe-Kuo direction numbers as used by scipy.stats.qmc.Sobol(scramble=False)
  * (30 bits): poly[dim], vinit[dim][18] from scipy's
  * _sobol_direction_numbers.npz -> v_out[30][dim] (HOST).  Point n of the

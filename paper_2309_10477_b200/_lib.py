@@ -45,6 +45,7 @@ EXPORTS = (
     "hmc_sobol_quantile_check", "hmc_box_muller_check", "hmc_fp32_paths_check",
     "hmc_surface_acc_words", "hmc_surface_workspace_bytes", "hmc_surface_partials",
     "hmc_surface_finalize", "hmc_surface", "hmc_exact_batch_f64", "hmc_exact_runs_f64",
+    "hmc_exact_greeks_chunks",
 )
 HMC_SURF_MAX_STRIKES = 128
 HMC_SURF_MAX_MATS = 32
@@ -120,6 +121,7 @@ def _declare(L: ctypes.CDLL) -> None:
         "hmc_surface": (ctypes.c_int, [pM, ctypes.POINTER(SurfaceSpec), pS, pd, i32]),
         "hmc_exact_batch_f64": (ctypes.c_int, [pM, dbl, pd, i32, ctypes.POINTER(i64), i64, i64, u64,
                                                pd, pd, i32]),
+        "hmc_exact_greeks_chunks": (ctypes.c_int, [pM, pP, pS, pd, i32, ctypes.POINTER(i64), vp, vp]),
         "hmc_exact_runs_f64": (ctypes.c_int, [pM, dbl, pd, i32, ctypes.POINTER(i64), i64, i64,
                                               ctypes.POINTER(u64), i32, pd,
                                               ctypes.POINTER(ctypes.c_uint32), i32, i64, pd, i32]),

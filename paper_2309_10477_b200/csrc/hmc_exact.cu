@@ -348,7 +348,8 @@ __global__ void __launch_bounds__(kExactThreads, MINB) exact_batch_kernel(const 
         // 1..N under per-(run, dimension) digital shifts (randomised QMC)
         uint32_t gray = 0;
         if (e.sobol_v) {
-            const uint32_t idx = (uint32_t)(1 + (e.sobol_scramble ? 0LL : run * e.sobol_n_paths) + e.path_lo + p);
+            const uint32_t idx = (uint32_t)(1 + (e.sobol_scramble ? 0LL : (e.run_offset + run) * e.sobol_n_paths) +
+                                            e.path_lo + p);
             gray = idx ^ (idx >> 1);
         }
         for (int k = 0; k < e.n_steps; ++k) {
@@ -411,6 +412,53 @@ __global__ void __launch_bounds__(kExactThreads, MINB) exact_batch_kernel(const 
         e.out[3 * i + 1] = price_sum / e.n_dates;
         e.out[3 * i + 2] = tw_sum / e.n_dates;
     }
+}
+
+// Per-path estimators of the exact scheme on the device (the engine's
+// greeks_epilogue, fp64) from the observables of the base and bumped
+// simulations, reduced per 128-path tile like the discretised kernels --
+// so exact-scheme jobs use the same chunk exchange and fixed-shape run
+// reduction (bit-identical for any number of GPUs).
+//   obs*: [run][n][3] (s_T, avg, tw_sum); U/D: v0 +- bumps; P/M: r +- h_r
+//   (Asian only; European r bumps rescale S_T by e^{+-h T}).
+__global__ void __launch_bounds__(kTile) exact_estimator_kernel(const KernelArgs a, const double* __restrict__ o0,
+                                                                const double* __restrict__ oU,
+                                                                const double* __restrict__ oD,
+                                                                const double* __restrict__ oP,
+                                                                const double* __restrict__ oM, long long n,
+                                                                double ehT, double emhT, double* __restrict__ tiles,
+                                                                long long n_tiles, int run0) {
+    const int run = blockIdx.y;
+    const long long i = (long long)blockIdx.x * kTile + threadIdx.x;
+    const bool live = i < n;
+    const size_t row = ((size_t)run * n + (live ? i : 0)) * 3;
+    const int col = a.is_asian ? 1 : 0;
+    const double A = o0[row + col], tw = o0[row + 2];
+    double Au = A, Ad = A, Rp = A * ehT, Rm = A * emhT;
+    if (a.want_greeks) {
+        Au = oU[row + col];
+        Ad = oD[row + col];
+        if (a.is_asian) {
+            Rp = oP[row + 1];
+            Rm = oM[row + 1];
+        }
+    }
+    double q[kNQ];
+    greeks_epilogue<double>(a, A, tw, Au, Ad, Rp, Rm, q);
+    if (!live) {
+#pragma unroll
+        for (int k = 0; k < kNQ; ++k) q[k] = 0.0;
+    }
+    tile_reduce_store(q, tiles + ((size_t)(run0 + run) * n_tiles + blockIdx.x) * kNW);
+}
+
+cudaError_t launch_exact_estimators(const KernelArgs& a, const double* const obs[5], long long n, int n_runs,
+                                    double ehT, double emhT, double* tiles, long long n_tiles, int run0,
+                                    cudaStream_t s) {
+    dim3 grid((unsigned)((n + kTile - 1) / kTile), (unsigned)n_runs);
+    exact_estimator_kernel<<<grid, kTile, 0, s>>>(a, obs[0], obs[1], obs[2], obs[3], obs[4], n, ehT, emhT, tiles,
+                                                  n_tiles, run0);
+    return cudaGetLastError();
 }
 
 cudaError_t exact_plan(long long rows, int sms, int* grid, int* variant) {

@@ -78,6 +78,7 @@ struct ExactArgs {
     long long path_lo, path_hi;
     const unsigned long long* key_runs;  // [n_runs] per-run stream keys (device)
     int n_runs;
+    int run_offset;          // global index of run 0 of this launch (Sobol blocks)
     const double* uniforms;  // [n_runs][n][3 n_steps] or null
     const uint32_t* sobol_v; // [30][3 n_steps] Sobol direction numbers (device) or null
     int sobol_scramble;      // digital shifts per (run, dimension)
@@ -91,6 +92,10 @@ struct ExactArgs {
 // (run, path) pairs; the node cache is sized by grid * kExactThreads
 cudaError_t exact_plan(long long rows, int sms, int* grid, int* variant);
 cudaError_t launch_exact(const ExactArgs& e, int grid, int variant, cudaStream_t s);
+// per-path exact-scheme estimators -> tiles[run0 + run][tile][HMC_NW]
+cudaError_t launch_exact_estimators(const KernelArgs& a, const double* const obs[5], long long n, int n_runs,
+                                    double ehT, double emhT, double* tiles, long long n_tiles, int run0,
+                                    cudaStream_t s);
 
 // the production step arithmetic on given normals (hmc_fast.cu), per path
 cudaError_t launch_given_normals(const KernelArgs& a, const float2* d_z, long long n, double* d_out,

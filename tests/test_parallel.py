@@ -91,66 +91,3 @@ def test_gather_world2_matches_single(n):
     # and therefore the fixed-order reduction is bit-identical across G
     np.testing.assert_array_equal(_seq_reduce(torch.tensor(got[1])), _seq_reduce(torch.tensor(single)))
 
-
-def _fake_exact_runs(params, s0, times, flags, path_lo, path_hi, key_runs, uniforms, sobol=None):
-    """CPU stand-in for cuda_backend.exact_runs: deterministic per-path
-    observables of (key_run, global path index, model)."""
-    idx = np.arange(path_lo, path_hi, dtype=np.float64)
-    out = []
-    for k in key_runs:
-        ph = (int(k) % 1000) * 1e-3 + params.v0 * 10.0
-        s_t = s0 * np.exp(0.2 * np.sin(idx * 0.37 + ph))
-        avg = s0 * np.exp(0.1 * np.cos(idx * 0.11 + ph))
-        out.append(np.stack([s_t, avg, 0.5 * avg], axis=1))
-    return np.array(out).reshape(len(key_runs), path_hi - path_lo, 3)
-
-
-def _exact_worker(rank, world, port, n, q):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    torch.distributed.init_process_group("gloo", rank=rank, world_size=world)
-    try:
-        from paper_2309_10477_b200 import OptionSpec, SimConfig, cuda_backend, engine, exact
-        from paper_2309_10477_b200.model import BENCH_PARAMS, HestonParams
-        cuda_backend.exact_runs = _fake_exact_runs
-        p = HestonParams(**BENCH_PARAMS)
-        out = {}
-        for spec in (OptionSpec("european", "call", 100.0, 1.0, 100.0),
-                     OptionSpec("asian_arithmetic", "call", 100.0, 1.0, 100.0,
-                                averaging_times=(0.25, 0.5, 0.75, 1.0))):
-            cfg = SimConfig(scheme="exact", n_paths=n, n_steps=1, n_runs=3, seed=9)
-            out[spec.style] = exact.execute(p, spec, cfg, True, engine.bump_sizes(p, spec, cfg))
-        q.put((rank, out))
-    finally:
-        torch.distributed.destroy_process_group()
-
-
-@pytest.mark.parametrize("n", [3 * HMC_CHUNK + 4096 + 77, 2 * 4096])
-def test_exact_scheme_world2_matches_single(n):
-    """The exact scheme's cross-rank exchange (reference 4096-path job
-    partials, all-gathered in path order, fsum per run) gives every rank
-    the single-process sums bit for bit."""
-    from paper_2309_10477_b200 import OptionSpec, SimConfig, cuda_backend, engine, exact
-    from paper_2309_10477_b200.model import BENCH_PARAMS, HestonParams
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_exact_worker, args=(r, 2, port, n, q)) for r in range(2)]
-    for p in procs:
-        p.start()
-    got = dict(q.get(timeout=180) for _ in procs)
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
-    orig = cuda_backend.exact_runs
-    cuda_backend.exact_runs = _fake_exact_runs
-    try:
-        p = HestonParams(**BENCH_PARAMS)
-        for spec in (OptionSpec("european", "call", 100.0, 1.0, 100.0),
-                     OptionSpec("asian_arithmetic", "call", 100.0, 1.0, 100.0,
-                                averaging_times=(0.25, 0.5, 0.75, 1.0))):
-            cfg = SimConfig(scheme="exact", n_paths=n, n_steps=1, n_runs=3, seed=9)
-            single = exact.execute(p, spec, cfg, True, engine.bump_sizes(p, spec, cfg))
-            for r in (0, 1):
-                np.testing.assert_array_equal(got[r][spec.style], single)
-    finally:
-        cuda_backend.exact_runs = orig
