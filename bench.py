@@ -65,7 +65,7 @@ def secondary_workloads(reps: int = 3, sm_mhz: float = 1965.0) -> dict:
     import numpy as np
     import torch
     from paper_2309_10477_b200 import (BENCH_PARAMS, HestonParams, OptionSpec, SimConfig, greeks,
-                                       surface, daily_fixings)
+                                       price, surface, daily_fixings)
     p = HestonParams(**BENCH_PARAMS)
     euro = OptionSpec("european", "call", 100.0, 1.0, 100.0)
     asian = OptionSpec("asian_arithmetic", "call", 100.0, 1.0, 100.0,
@@ -85,6 +85,9 @@ def secondary_workloads(reps: int = 3, sm_mhz: float = 1965.0) -> dict:
                                                sobol_bridge=16, n_paths=2**22, n_steps=252,
                                                n_runs=1, seed=7)),
             2**22 * 252),
+        "exact_bk_european_price_2^17": (      # compare with cpu_baseline_exact (price only)
+            lambda: price(p, euro, SimConfig(scheme="exact", n_paths=2**17, n_steps=1, n_runs=1,
+                                             seed=7)), 2**17),
         "exact_bk_european_full_greeks_2^17": (
             lambda: greeks(p, euro, SimConfig(scheme="exact", n_paths=2**17, n_steps=1, n_runs=1,
                                               seed=7)), 2**17),
