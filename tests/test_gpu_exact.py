@@ -10,7 +10,7 @@ import pytest
 
 from conftest import GOLDEN
 from paper_2309_10477_b200 import (BesselNonConvergence, HestonParams, OptionSpec, SimConfig,
-                                   cuda_backend, price)
+                                   UnsupportedProduct, cuda_backend, greeks, price)
 from paper_2309_10477_b200.model import BENCH_PARAMS
 
 pytestmark = pytest.mark.gpu
@@ -107,3 +107,18 @@ def test_exact_device_sobol_equals_host_points(params, scramble):
             u = sobol.points(12, 1 + r * N + lo, hi - lo)
         host = cuda_backend.exact_batch(params, 100.0, times, flags, lo, hi, k, u)
         np.testing.assert_array_equal(dev[r], host)
+
+
+@pytest.mark.parametrize("sampler", ["pseudo", "sobol"])
+def test_exact_put_call_parity_and_price_only(params, sampler):
+    """Puts price on the exact scheme (price only, like the reference);
+    with common random numbers C - P = disc (S_T - K) path by path, so the
+    parity gap is the martingale error of the discounted S_T."""
+    cfg = SimConfig(scheme="exact", sampler=sampler, n_paths=2**15, n_steps=1, n_runs=4, seed=3)
+    c = price(params, OptionSpec("european", "call", 100.0, 1.0, 100.0), cfg)
+    p = price(params, OptionSpec("european", "put", 100.0, 1.0, 100.0), cfg)
+    gap = np.array(c.per_run_values) - np.array(p.per_run_values)
+    fwd = 100.0 - 100.0 * np.exp(-params.r)
+    assert np.all(np.abs(gap - fwd) < 0.5), gap
+    with pytest.raises(UnsupportedProduct):       # reference engine.py:120-121
+        greeks(params, OptionSpec("european", "put", 100.0, 1.0, 100.0), cfg)
