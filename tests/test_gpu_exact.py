@@ -122,3 +122,38 @@ def test_exact_put_call_parity_and_price_only(params, sampler):
     assert np.all(np.abs(gap - fwd) < 0.5), gap
     with pytest.raises(UnsupportedProduct):       # reference engine.py:120-121
         greeks(params, OptionSpec("european", "put", 100.0, 1.0, 100.0), cfg)
+
+
+def test_exact_chunks_split_bit_identical(params):
+    """hmc_exact_greeks_chunks on chunk-aligned slices produces the same
+    chunk partials as on the whole range: the exact scheme inherits the
+    engine's bit-identical multi-GPU reduction."""
+    import ctypes
+    import torch
+    from paper_2309_10477_b200 import _lib, engine, exact
+    spec = OptionSpec("asian_arithmetic", "call", 100.0, 1.0, 100.0, averaging_times=(0.25, 0.5, 0.75, 1.0))
+    cfg = SimConfig(scheme="exact", n_paths=3 * 16384 + 1000, n_steps=1, n_runs=2, seed=9)
+    h, vu, vd, hr = engine.bump_sizes(params, spec, cfg)
+    times = exact.exact_step_times(spec)
+    flags = np.ones(times.size - 1, dtype=np.int64)
+    L = _lib.lib()
+    m = _lib.Model(params.kappa, params.theta, params.sigma, params.rho, params.r, params.v0)
+    idx = np.zeros(1, dtype=np.int64)
+    pr = _lib.Product(1, 0, 100.0, 1.0, 100.0, idx.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), 1)
+    stream = torch.cuda.current_stream()
+
+    def chunks(lo, hi):
+        sim = _lib.Sim(scheme=2, sampler=0, precision=1, want_greeks=1, n_steps=4, n_runs=2,
+                       n_paths=cfg.n_paths, path_lo=lo, path_hi=hi, seed=9, h_spot=h, v0_up=vu, v0_dn=vd,
+                       h_r=hr)
+        nc = -(-(hi - lo) // 16384)
+        out = torch.empty((2, nc, _lib.HMC_NW), dtype=torch.float64, device="cuda")
+        _lib.check(L.hmc_exact_greeks_chunks(ctypes.byref(m), ctypes.byref(pr), ctypes.byref(sim),
+                                             times.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), 4,
+                                             flags.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                             ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(stream.cuda_stream)))
+        return out.cpu().numpy()
+
+    whole = chunks(0, cfg.n_paths)
+    parts = np.concatenate([chunks(0, 16384), chunks(16384, 3 * 16384), chunks(3 * 16384, cfg.n_paths)], axis=1)
+    np.testing.assert_array_equal(whole, parts)
