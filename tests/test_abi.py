@@ -152,3 +152,24 @@ def test_greeks_multi_validates_before_device_work():
     m, pr, sim, _keep = _job(right=1)
     assert L.hmc_greeks_multi(ctypes.byref(m), ctypes.byref(pr), ctypes.byref(sim),
                               out.ctypes.data_as(pd), devs, 2) == _lib.HMC_E_UNSUPPORTED
+
+
+@pytest.mark.parametrize("over,code", [(dict(right=1), _lib.HMC_E_UNSUPPORTED), (dict(path_lo=5), _lib.HMC_E_INVALID),
+                                       (dict(sampler=1), _lib.HMC_E_INVALID), (dict(h_r=0.0), _lib.HMC_E_INVALID)])
+def test_exact_greeks_chunks_validates_on_host(over, code):
+    L = _lib.lib()
+    right = over.pop("right", 0)
+    m = _lib.Model(2.0, 0.04, 0.3, -0.7, 0.03, 0.04)
+    idx = np.zeros(1, dtype=np.int64)
+    pr = _lib.Product(0, right, 100.0, 1.0, 100.0, idx.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), 1)
+    kw = dict(scheme=2, sampler=0, precision=1, want_greeks=1, n_steps=1, n_runs=1, n_paths=4096, path_lo=0,
+              path_hi=4096, seed=1, h_spot=0.5, v0_up=0.0404, v0_dn=0.0396, h_r=1e-4)
+    kw.update(over)
+    sim = _lib.Sim(**kw)
+    t = np.array([0.0, 1.0])
+    f = np.ones(1, dtype=np.int64)
+    buf = ctypes.create_string_buffer(64)
+    rc = L.hmc_exact_greeks_chunks(ctypes.byref(m), ctypes.byref(pr), ctypes.byref(sim),
+                                   t.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), 1,
+                                   f.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), buf, None)
+    assert rc == code
