@@ -20,7 +20,7 @@ struct SurfPrepared {
     std::vector<float> strikes;
     std::vector<hmc::SurfMat> mats;
     hmc::SurfArgs s{};
-    size_t off_st64 = 0, off_st32 = 0, off_k = 0, off_m = 0, bytes = 0;
+    size_t off_st64 = 0, off_st32 = 0, off_k = 0, off_m = 0, off_sobol = 0, bytes = 0;
 };
 
 int check_surface_spec(const hmc_surface_spec* sp, const hmc_sim* sim) {
@@ -40,8 +40,10 @@ int check_surface_spec(const hmc_surface_spec* sp, const hmc_sim* sim) {
             return fail(HMC_E_INVALID, "maturity grid indices must be >= 1 and strictly increasing");
     if (sim->n_steps != sp->mat_idx[sp->n_mats - 1])
         return fail(HMC_E_INVALID, "sim->n_steps must equal the last maturity's grid index");
-    if (sim->sampler != HMC_SAMPLER_PSEUDO || sim->precision != HMC_PREC_FP32)
-        return fail(HMC_E_UNSUPPORTED, "surfaces run on the fp32 pseudo-random path");
+    if (sim->precision != HMC_PREC_FP32)
+        return fail(HMC_E_UNSUPPORTED, "surfaces run on the fp32 path (pseudo or Sobol)");
+    if (sim->sobol_bridge != 0)
+        return fail(HMC_E_UNSUPPORTED, "surfaces take time-ordered Sobol dimensions (no bridge)");
     return HMC_OK;
 }
 
@@ -100,6 +102,9 @@ int prepare_surface(const hmc_model* m, const hmc_surface_spec* sp, const hmc_si
     off += align_up(S.strikes.size() * sizeof(float));
     S.off_m = off;
     off += align_up(S.mats.size() * sizeof(hmc::SurfMat));
+    S.off_sobol = off;
+    if (sim.sampler == HMC_SAMPLER_SOBOL && !sim.sobol_v_on_device)
+        off += align_up((size_t)30 * 2 * sim.n_steps * sizeof(uint32_t));
     S.bytes = off;
     return HMC_OK;
 }
@@ -121,10 +126,13 @@ int64_t hmc_surface_acc_words(const hmc_surface_spec* spec, int32_t n_runs) {
 
 int64_t hmc_surface_workspace_bytes(const hmc_surface_spec* spec, const hmc_sim* sim) {
     if (!spec || !sim || sim->n_steps < 1) return 0;
-    return (int64_t)(align_up(((size_t)sim->n_steps + 1) * sizeof(StepD)) +
-                     align_up(((size_t)sim->n_steps + 1) * sizeof(float4)) +
-                     align_up((size_t)spec->n_strikes * sizeof(float)) +
-                     align_up((size_t)spec->n_mats * sizeof(hmc::SurfMat)));
+    size_t b = align_up(((size_t)sim->n_steps + 1) * sizeof(StepD)) +
+               align_up(((size_t)sim->n_steps + 1) * sizeof(float4)) +
+               align_up((size_t)spec->n_strikes * sizeof(float)) +
+               align_up((size_t)spec->n_mats * sizeof(hmc::SurfMat));
+    if (sim->sampler == HMC_SAMPLER_SOBOL && !sim->sobol_v_on_device)
+        b += align_up((size_t)30 * 2 * sim->n_steps * sizeof(uint32_t));
+    return (int64_t)b;
 }
 
 int hmc_surface_partials(const hmc_model* model, const hmc_surface_spec* spec, const hmc_sim* sim,
@@ -148,6 +156,15 @@ int hmc_surface_partials(const hmc_model* model, const hmc_surface_spec* spec, c
     S.s.strikes = (const float*)(w + S.off_k);
     S.s.mats = (const hmc::SurfMat*)(w + S.off_m);
     S.s.acc = (unsigned long long*)d_acc;
+    if (sim->sampler == HMC_SAMPLER_SOBOL) {
+        if (sim->sobol_v_on_device) {
+            S.P.a.sobol_v = sim->sobol_v;
+        } else {
+            HMC_CK(cudaMemcpyAsync(w + S.off_sobol, sim->sobol_v, (size_t)30 * S.P.a.sobol_dim * sizeof(uint32_t),
+                                   cudaMemcpyHostToDevice, st));
+            S.P.a.sobol_v = (const uint32_t*)(w + S.off_sobol);
+        }
+    }
     const long long n_tiles = (sim->path_hi - sim->path_lo + hmc::kSurfThreads - 1) / hmc::kSurfThreads;
     int dev = 0, sms = 148;
     HMC_CK(cudaGetDevice(&dev));

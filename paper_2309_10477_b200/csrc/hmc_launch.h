@@ -36,7 +36,7 @@ constexpr int kSurfMaxMats = HMC_SURF_MAX_MATS;
 constexpr int kSurfVals = 23;
 constexpr int kSurfBucketRows = 15;
 constexpr float kSurfLinScale = 1024.0f;      // 2^10 fixed point for linear moments
-constexpr float kSurfQuadScale = 0.25f;       // 2^-2 for quadratic moments
+constexpr float kSurfQuadScale = 4.0f;        // 2^2 for quadratic moments (A^2 >= 2^18 escapes to int64)
 constexpr float kSurfBandScale = 1048576.0f;  // 2^20 for the (small, <= ~1) band moments
 
 struct SurfMat {

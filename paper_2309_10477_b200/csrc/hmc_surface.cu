@@ -26,6 +26,7 @@
 #include "hmc_launch.h"
 
 #include "hmc_path32.cuh"
+#include "hmc_sobol32.cuh"
 
 namespace hmc {
 
@@ -155,6 +156,13 @@ __device__ __forceinline__ void surface_checkpoint(const PathState32& st, const 
     __syncthreads();
 }
 
+// Sobol surfaces: the path kernel's Gray-code tables sized for the
+// surface block (kSurfThreads / 32 warps), 32 steps per refill (the static
+// shared-memory budget is 48 KB)
+constexpr int kSurfSobolSteps = 32;
+using SurfSobolTables = SobolTablesT<kSurfSobolSteps, kSurfThreads / 32>;
+
+template <int SAMPLER>
 __global__ void __launch_bounds__(kSurfThreads, kSurfMinBlocks) surface_kernel(const KernelArgs a, const SurfArgs s,
                                                                   long long n_tiles) {
     extern __shared__ int hist[];  // [2][kSurfVals][nK + 1] int32 fixed point
@@ -184,6 +192,31 @@ __global__ void __launch_bounds__(kSurfThreads, kSurfMinBlocks) surface_kernel(c
         st.A0 = st.Au = st.Ad = 0.0f;
         st.T1 = st.Dp = st.Dm = 0.0f;
         int m = 0, next = s.mats[0].step;
+        if (SAMPLER == HMC_SAMPLER_SOBOL) {
+            // the single-product Sobol driver's points and quantile (same
+            // dimensions 2(k-1), 2(k-1)+1 per step), checkpoints in between
+            __shared__ SurfSobolTables tab;
+            const SobolLane sl(run, live ? path : a.path_lo, a);
+            const float c1 = kSqrt2f * a.f_sqdt * a.f_log2e, cs = kSqrt2f * a.f_sigma * a.f_sqdt;
+#pragma unroll 1
+            for (int k0 = 1; k0 <= a.n_sim; k0 += kSurfSobolSteps) {
+                const int mq = min(kSurfSobolSteps, a.n_sim - k0 + 1);
+                sobol_refill(tab, k0 - 1, mq, sl, a);
+#pragma unroll 1
+                for (int q = 0; q < mq; ++q) {
+                    const int k = k0 + q;
+                    float za, zb;
+                    sobol_pair(tab, q, sl, za, zb);
+                    step<kFixEvery, true>(st, k, c1 * za, cs * fmaf(a.f_rho, za, a.f_sq1mr2 * zb), a);
+                    if (k == next) {
+                        surface_checkpoint(st, a, s, m, live, hist, sK, pow2, gacc);
+                        ++m;
+                        next = m < s.n_mats ? s.mats[m].step : 0x7fffffff;
+                    }
+                }
+            }
+            continue;
+        }
 #pragma unroll 1
         for (int k0 = 1; k0 <= a.n_sim; k0 += 3) {
             // same Philox counters as fast_greeks_kernel: (step triple, path, key_run)
@@ -220,11 +253,11 @@ __global__ void __launch_bounds__(kSurfThreads, kSurfMinBlocks) surface_kernel(c
 cudaError_t launch_surface(const KernelArgs& a, const SurfArgs& s, long long n_tiles, int grid_x,
                            cudaStream_t stream) {
     const size_t smem = (size_t)2 * kSurfVals * (s.nK + 1) * sizeof(int);
-    cudaError_t e = cudaFuncSetAttribute(surface_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    auto k = a.sampler == HMC_SAMPLER_SOBOL ? surface_kernel<HMC_SAMPLER_SOBOL> : surface_kernel<HMC_SAMPLER_PSEUDO>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid((unsigned)grid_x, (unsigned)a.n_runs);
-    surface_kernel<<<grid, kSurfThreads, smem, stream>>>(a, s, n_tiles);
+    k<<<grid, kSurfThreads, smem, stream>>>(a, s, n_tiles);
     return cudaGetLastError();
 }
 

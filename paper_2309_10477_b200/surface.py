@@ -23,7 +23,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import _lib, parallel
+from . import _lib, parallel, sobol
 from .errors import DeviceError, UnsupportedProduct, ValidationError
 from .model import GridSpec, HestonParams, OptionSpec, SimConfig
 
@@ -58,8 +58,10 @@ class SurfaceJob:
                  spot: float = 100.0):
         if config.scheme == "exact":
             raise UnsupportedProduct("surfaces run on the euler / milstein schemes")
-        if config.sampler != "pseudo" or config.precision != "fp32":
-            raise UnsupportedProduct("surfaces run on the fp32 pseudo-random path")
+        if config.precision != "fp32":
+            raise UnsupportedProduct("surfaces run on the fp32 path (pseudo or Sobol)")
+        if config.sobol_bridge:
+            raise UnsupportedProduct("surfaces take time-ordered Sobol dimensions (no Brownian bridge)")
         self.strikes = np.ascontiguousarray(strikes, dtype=np.float64)
         if not (1 <= self.strikes.size <= _lib.HMC_SURF_MAX_STRIKES):
             raise ValidationError(f"need 1..{_lib.HMC_SURF_MAX_STRIKES} strikes")
@@ -79,11 +81,17 @@ class SurfaceJob:
         self.model = _lib.Model(params.kappa, params.theta, params.sigma, params.rho, params.r,
                                 params.v0)
         self.sim = _lib.Sim(
-            scheme=_lib.SCHEME[config.scheme], sampler=0, precision=0, want_greeks=1,
+            scheme=_lib.SCHEME[config.scheme], sampler=_lib.SAMPLER[config.sampler], precision=0,
+            want_greeks=1, sobol_scramble=int(bool(config.sobol_scramble)),
             n_steps=config.n_steps, n_runs=config.n_runs, n_paths=config.n_paths, path_lo=0,
             path_hi=config.n_paths, seed=config.seed & (2**64 - 1), h_spot=config.bump_spot * spot,
             v0_up=params.v0 + hv, v0_dn=max(params.v0 - hv, 0.0), h_r=config.bump_r)
         self.config = config
+        self._directions = None
+        if config.sampler == "sobol":   # the single-product engine's points (engine.py:97-101)
+            self._directions = np.ascontiguousarray(sobol.directions(2 * config.n_steps))
+            self.sim.sobol_v = self._directions.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))
+            self.sim.sobol_v_on_device = 0
 
     def run_device(self, group=None) -> np.ndarray:
         """Accumulate this rank's slice, all-reduce the int64 histograms,

@@ -26,15 +26,19 @@ def _cfg(n_steps, **kw):
     return SimConfig(**base)
 
 
-def test_surface_points_equal_single_product_engine():
+@pytest.mark.parametrize("qmc", [{}, dict(sampler="sobol", sobol_highdim_ack=True),
+                                 dict(sampler="sobol", sobol_highdim_ack=True, sobol_scramble=True)])
+def test_surface_points_equal_single_product_engine(qmc):
+    """Pseudo-random and (randomised) Sobol surfaces: every point equals the
+    single-product engine on the same paths / points."""
     p = HestonParams(**BENCH_PARAMS)
-    res = surface(p, STRIKES, MATS, _cfg(64))
+    res = surface(p, STRIKES, MATS, _cfg(64, **qmc))
     for mi, T in enumerate(MATS):
         n = int(round(T * 64))
         for j, K in enumerate(STRIKES):
             for style in ("european", "asian_arithmetic"):
                 dates = daily_fixings(T, n) if style != "european" else ()
-                g = greeks(p, OptionSpec(style, "call", K, T, 100.0, averaging_times=dates), _cfg(n))
+                g = greeks(p, OptionSpec(style, "call", K, T, 100.0, averaging_times=dates), _cfg(n, **qmc))
                 for q in QN:
                     est = res.estimate[style][q][mi, j]
                     # Vega differences two separately accumulated fp32 averages
@@ -43,7 +47,10 @@ def test_surface_points_equal_single_product_engine():
                     assert abs(est - g[q].estimate) <= tol * scale + 1e-6, (style, T, K, q, est,
                                                                            g[q].estimate)
                     se, se_ref = res.path_std_error[style][q][mi, j], g[q].path_std_error
-                    assert abs(se - se_ref) <= 2e-2 * se_ref + 1e-7, (style, T, K, q, se, se_ref)
+                    # second moments come from fixed-point histograms (A at 2^-10, A^2 at
+                    # 2^-2 resolution): ~1e-6 absolute on an SE, visible only at deep-OTM
+                    # points whose SE is itself ~1e-5
+                    assert abs(se - se_ref) <= 2e-2 * se_ref + 2e-6, (style, T, K, q, se, se_ref)
 
 
 def test_split_paths_bit_identical():

@@ -11,7 +11,7 @@ import pytest
 
 from paper_2309_10477_b200 import _lib
 
-LIN, QUAD, BAND = 1024.0, 0.25, 1048576.0  # hmc_launch.h kSurf*Scale
+LIN, QUAD, BAND = 1024.0, 4.0, 1048576.0  # hmc_launch.h kSurf*Scale
 ROWS = 23
 
 
