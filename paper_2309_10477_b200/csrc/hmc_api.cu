@@ -385,14 +385,18 @@ __global__ void box_muller_kat_kernel(const uint4* __restrict__ w, int n, Kernel
     }
 }
 
-// the production kernels' Sobol quantile on given 30-bit coordinates
+// the production kernels' Sobol quantile on given 30-bit coordinates: the
+// paired form (x[i], x[n-1-i]) as the path kernels use it, its second lane
+// checked bit for bit against the scalar form (a mismatch writes NaN).
+// Every lane of a warp runs the quantile (its tail branches are warp votes).
 __global__ void sobol_quantile_kernel(const uint32_t* __restrict__ x, int n, float half,
                                       float* __restrict__ out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) {
-        const float ht = half * 9.31322574615478515625e-10f;
-        out[i] = kSqrt2f * sobol_normal_u(x[i], 2.0f * ht, ht);
-    }
+    const int j = min(i, n - 1);
+    const float ht = half * 9.31322574615478515625e-10f;
+    const float2 z = sobol_normal_u2(x[j], x[n - 1 - j], 2.0f * ht, ht);
+    const float s = sobol_normal_u(x[n - 1 - j], 2.0f * ht, ht);
+    if (i < n) out[i] = __float_as_uint(s) == __float_as_uint(z.y) ? kSqrt2f * z.x : __int_as_float(0x7fffffff);
 }
 
 cudaError_t launch_chunks_to_runs(const double* d_chunks, long long n_chunks, int n_runs,

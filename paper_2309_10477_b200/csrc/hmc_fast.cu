@@ -60,7 +60,7 @@ constexpr int kSamplerBridge = 2;  // internal: Sobol with Brownian-bridge order
 template <int FIX, bool GREEKS>
 __device__ __forceinline__ void sobol_paths(PathState32& st, int run, long long p, const KernelArgs& a) {
     __shared__ SobolTables tab;
-    const SobolLane sl(run, p, a);
+    const SobolLane sl(run, p, a.path_lo + (long long)blockIdx.x * kTile, kWarps, a);
     const float c1 = kSqrt2f * a.f_sqdt * a.f_log2e;  // sobol_pair returns z / sqrt(2)
     const float cs = kSqrt2f * a.f_sigma * a.f_sqdt;
 
@@ -74,7 +74,7 @@ __device__ __forceinline__ void sobol_paths(PathState32& st, int run, long long 
             sobol_pair(tab, q, sl, za, zb);
             const float z1l = c1 * za;
             const float sz2 = cs * fmaf(a.f_rho, za, a.f_sq1mr2 * zb);
-            step<FIX, GREEKS>(st, k0 + q, z1l, sz2, a);
+            step<FIX, GREEKS, true>(st, k0 + q, z1l, sz2, a);
         }
     }
 }
@@ -92,7 +92,7 @@ __device__ __forceinline__ void sobol_bridge_paths(PathState32& st, int run, lon
     __shared__ SobolTablesT<kQ, kWarps> tab;
     extern __shared__ float2 skel[];
     float2* my = skel + threadIdx.x;  // point j at my[j * kTile]
-    const SobolLane sl(run, p, a);
+    const SobolLane sl(run, p, a.path_lo + (long long)blockIdx.x * kTile, kWarps, a);
     const int S = a.bridge_segments;
     const float l2e = a.f_log2e, sg = a.f_sigma;
 
@@ -142,7 +142,7 @@ __device__ __forceinline__ void sobol_bridge_paths(PathState32& st, int run, lon
             j = min(j + 1, S);
             R = my[j * kTile];
         }
-        step<FIX, GREEKS>(st, k, l2e * d1, sg * fmaf(a.f_rho, d1, a.f_sq1mr2 * d2), a);
+        step<FIX, GREEKS, true>(st, k, l2e * d1, sg * fmaf(a.f_rho, d1, a.f_sq1mr2 * d2), a);
     }
 }
 
@@ -162,10 +162,9 @@ __global__ void HMC_BOUNDS fast_greeks_kernel(const KernelArgs a,
 #endif
     PathState32 st;
     st.v0 = a.f_v0;
-    st.vu = a.f_vu;
-    st.vd = a.f_vd;
-    st.L0 = st.Lu = st.Ld = 0.0f;
-    st.A0 = st.Au = st.Ad = 0.0f;
+    st.vb = make_float2(a.f_vu, a.f_vd);
+    st.L0 = st.A0 = 0.0f;
+    st.Lb = st.Ab = make_float2(0.0f, 0.0f);
     st.T1 = st.Dp = st.Dm = 0.0f;
 
     if (SAMPLER == HMC_SAMPLER_PSEUDO) {
@@ -185,7 +184,7 @@ __global__ void HMC_BOUNDS fast_greeks_kernel(const KernelArgs a,
             for (int i = 0; i < 3; ++i) {
                 float z1l, sz2;
                 box_muller_f(fr[i], fa[i], x.x << (31 - i), a, z1l, sz2);
-                step<FIX, GREEKS>(st, k + i, z1l, sz2, a);
+                step<FIX, GREEKS, FIX == kFixLast>(st, k + i, z1l, sz2, a);
             }
             k += 3;
         }
@@ -196,7 +195,7 @@ __global__ void HMC_BOUNDS fast_greeks_kernel(const KernelArgs a,
             for (int i = 0; k + i <= a.n_sim; ++i) {
                 float z1l, sz2;
                 box_muller_f(fr[i], fa[i], x.x << (31 - i), a, z1l, sz2);
-                step<FIX, GREEKS>(st, k + i, z1l, sz2, a);
+                step<FIX, GREEKS, FIX == kFixLast>(st, k + i, z1l, sz2, a);
             }
         }
 #else
@@ -215,16 +214,16 @@ __global__ void HMC_BOUNDS fast_greeks_kernel(const KernelArgs a,
 #endif
             float z1l, sz2;
             box_muller(x.x, x.y, a, z1l, sz2);
-            step<FIX, GREEKS>(st, k, z1l, sz2, a);
+            step<FIX, GREEKS, FIX == kFixLast>(st, k, z1l, sz2, a);
             box_muller(x.z, x.w, a, z1l, sz2);
-            step<FIX, GREEKS>(st, k + 1, z1l, sz2, a);
+            step<FIX, GREEKS, FIX == kFixLast>(st, k + 1, z1l, sz2, a);
             k += 2;
         }
         if (a.n_sim & 1) {
             const uint4 x = philox4x32_10((uint32_t)npairs, c1, c2, c3);
             float z1l, sz2;
             box_muller(x.x, x.y, a, z1l, sz2);
-            step<FIX, GREEKS>(st, k, z1l, sz2, a);
+            step<FIX, GREEKS, FIX == kFixLast>(st, k, z1l, sz2, a);
         }
 #endif
     } else if (SAMPLER == HMC_SAMPLER_SOBOL) {
@@ -238,7 +237,7 @@ __global__ void HMC_BOUNDS fast_greeks_kernel(const KernelArgs a,
     const float A = st.A0 * inv_n;
     double q[kNQ];
     if (GREEKS) {
-        greeks_epilogue_f32(a, A, st.T1 * inv_n, st.Au * inv_n, st.Ad * inv_n, st.Dp * inv_n,
+        greeks_epilogue_f32(a, A, st.T1 * inv_n, st.Ab.x * inv_n, st.Ab.y * inv_n, st.Dp * inv_n,
                             st.Dm * inv_n, q);
     } else {
         const float K = a.f_K, disc = a.f_disc;
@@ -288,10 +287,9 @@ __global__ void __launch_bounds__(kTile) given_normals_kernel(const KernelArgs a
     if (i >= n) return;
     PathState32 st;
     st.v0 = a.f_v0;
-    st.vu = a.f_vu;
-    st.vd = a.f_vd;
-    st.L0 = st.Lu = st.Ld = 0.0f;
-    st.A0 = st.Au = st.Ad = 0.0f;
+    st.vb = make_float2(a.f_vu, a.f_vd);
+    st.L0 = st.A0 = 0.0f;
+    st.Lb = st.Ab = make_float2(0.0f, 0.0f);
     st.T1 = st.Dp = st.Dm = 0.0f;
     const float c1 = a.f_sqdt * a.f_log2e, cs = a.f_sigma * a.f_sqdt;
     for (int k = 1; k <= a.n_sim; ++k) {
@@ -302,7 +300,7 @@ __global__ void __launch_bounds__(kTile) given_normals_kernel(const KernelArgs a
     const float inv_n = a.f_inv_navg;
     const float A = st.A0 * inv_n;
     double q[kNQ];
-    greeks_epilogue_f32(a, A, st.T1 * inv_n, st.Au * inv_n, st.Ad * inv_n, st.Dp * inv_n, st.Dm * inv_n,
+    greeks_epilogue_f32(a, A, st.T1 * inv_n, st.Ab.x * inv_n, st.Ab.y * inv_n, st.Dp * inv_n, st.Dm * inv_n,
                         q);
 #pragma unroll
     for (int j = 0; j < kNQ; ++j) out[(size_t)i * kNQ + j] = q[j];

@@ -32,6 +32,9 @@
 #ifndef HMC_TRIPACK
 #define HMC_TRIPACK 1        // 3 steps per Philox block (23-bit radius, 19/18-bit angle)
 #endif
+#ifndef HMC_EX2_PAIR_POLY
+#define HMC_EX2_PAIR_POLY 0  // bumped pair's 2^L by a paired FMA polynomial instead of 2 MUFU.EX2
+#endif
 #ifndef HMC_UNROLL_PAIRS
 #define HMC_UNROLL_PAIRS 1
 #endif
@@ -70,6 +73,8 @@ __device__ __forceinline__ float sqrt_var(float v) {
 #endif
 }
 
+__device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
+
 // 2^x on the FMA pipe: x = j + f, |f| <= 1/2, 2^f by a degree-6 Taylor
 // polynomial (rel. err 1.6e-7), exponent added with one LEA.
 __device__ __forceinline__ float ex2_poly(float x) {
@@ -91,6 +96,23 @@ template <int POLY>
 __device__ __forceinline__ float ex2_sel(float x) {
     if (POLY) return ex2_poly(x);
     return ex2a(x);
+}
+
+// ex2_poly on a pair with paired FFMA2/FADD2 (the same per-lane arithmetic)
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+    const float magic = 12582912.0f;
+    x = make_float2(fmaxf(x.x, -125.0f), fmaxf(x.y, -125.0f));
+    const float2 m = __fadd2_rn(x, make_float2(magic, magic));
+    const float2 f = __ffma2_rn(__fadd2_rn(m, make_float2(-magic, -magic)), make_float2(-1.0f, -1.0f), x);
+    float2 p = make_float2(1.5403530393381606e-4f, 1.5403530393381606e-4f);
+    p = __ffma2_rn(p, f, make_float2(1.3333558146428441e-3f, 1.3333558146428441e-3f));
+    p = __ffma2_rn(p, f, make_float2(9.6181291076284772e-3f, 9.6181291076284772e-3f));
+    p = __ffma2_rn(p, f, make_float2(5.5504108664821576e-2f, 5.5504108664821576e-2f));
+    p = __ffma2_rn(p, f, make_float2(2.4022650695910071e-1f, 2.4022650695910071e-1f));
+    p = __ffma2_rn(p, f, make_float2(6.9314718055994531e-1f, 6.9314718055994531e-1f));
+    p = __ffma2_rn(p, f, make_float2(1.0f, 1.0f));
+    return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(m.x) << 23)),
+                       __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(m.y) << 23)));
 }
 
 // uniform in [1, 2) from the top 23 bits of x: one LEA.HI
@@ -274,12 +296,63 @@ __device__ __forceinline__ float sobol_normal_u(uint32_t x, float hx, float ht) 
 
 constexpr float kSqrt2f = 1.41421356237309504880f;
 
+#ifndef HMC_SOBOL_PAIR
+#define HMC_SOBOL_PAIR 1     // both coordinates of a step through one paired (FFMA2) quantile
+#endif
 
+// sobol_normal_u on two coordinates at once: the same per-lane arithmetic
+// (bit-identical results) with the float work as paired FADD2/FMUL2/FFMA2
+__device__ __forceinline__ float2 sobol_normal_u2(uint32_t xa, uint32_t xb, float hx, float ht) {
+    const bool ha = xa >= (1u << 29), hb = xb >= (1u << 29);
+    const uint32_t ta = ha ? (1u << 30) - xa : xa, tb = hb ? (1u << 30) - xb : xb;
+    const float2 xs = __ffma2_rn(make_float2((float)((int)(2u * xa) - (1 << 30)), (float)((int)(2u * xb) - (1 << 30))),
+                                 f2(9.31322574615478515625e-10f), f2(hx));
+    const float2 tf = __ffma2_rn(make_float2((float)ta, (float)tb), f2(9.31322574615478515625e-10f),
+                                 make_float2(ha ? -ht : ht, hb ? -ht : ht));
+    const float2 om = __ffma2_rn(tf, f2(-1.0f), f2(1.0f));                  // 1 - tf, one rounding
+    const float2 pr = __fmul2_rn(tf, om);
+    const float2 w = __ffma2_rn(make_float2(lg2a(pr.x), lg2a(pr.y)), f2(-0.69314718055994530942f),
+                                f2(-1.38629436111989061883f));
+    const float2 wc = __fadd2_rn(w, f2(-2.5f));
+    float2 p = f2(2.81022636e-08f);
+    p = __ffma2_rn(p, wc, f2(3.43273939e-07f));
+    p = __ffma2_rn(p, wc, f2(-3.5233877e-06f));
+    p = __ffma2_rn(p, wc, f2(-4.39150654e-06f));
+    p = __ffma2_rn(p, wc, f2(0.00021858087f));
+    p = __ffma2_rn(p, wc, f2(-0.00125372503f));
+    p = __ffma2_rn(p, wc, f2(-0.00417768164f));
+    p = __ffma2_rn(p, wc, f2(0.246640727f));
+    p = __ffma2_rn(p, wc, f2(1.50140941f));
+    if (__any_sync(0xffffffffu, fmaxf(w.x, w.y) >= 5.0f)) {
+        const float2 wt = __fadd2_rn(make_float2(sqrta(w.x), sqrta(w.y)), f2(-3.0f));
+        float2 q = f2(-0.000200214257f);
+        q = __ffma2_rn(q, wt, f2(0.000100950558f));
+        q = __ffma2_rn(q, wt, f2(0.00134934322f));
+        q = __ffma2_rn(q, wt, f2(-0.00367342844f));
+        q = __ffma2_rn(q, wt, f2(0.00573950773f));
+        q = __ffma2_rn(q, wt, f2(-0.0076224613f));
+        q = __ffma2_rn(q, wt, f2(0.00943887047f));
+        q = __ffma2_rn(q, wt, f2(1.00167406f));
+        q = __ffma2_rn(q, wt, f2(2.83297682f));
+        p.x = w.x >= 5.0f ? q.x : p.x;
+        p.y = w.y >= 5.0f ? q.y : p.y;
+        if (__any_sync(0xffffffffu, fmaxf(w.x, w.y) >= 16.0f)) {   // extreme cells: the scalar path
+            const float2 r = __fmul2_rn(p, xs);
+            const float sa = sobol_normal_u(xa, hx, ht), sb = sobol_normal_u(xb, hx, ht);  // all lanes
+            return make_float2(w.x >= 16.0f ? sa : r.x, w.y >= 16.0f ? sb : r.y);
+        }
+    }
+    return __fmul2_rn(p, xs);
+}
+
+
+// The two v0-bumped trajectories run as one float2 pair (.x: v0 + h, .y:
+// v0 - h floored at 0) so their updates issue as sm_100 paired FFMA2 --
+// the same IEEE fma per lane, half the issue slots.
 struct PathState32 {
-    float v0, L0, A0;  // base trajectory
-    float vu, Lu, Au;  // v0 + h
-    float vd, Ld, Ad;  // v0 - h (floored at 0)
-    float T1, Dp, Dm;  // base: sum S t, sum S expm1(h t), sum S expm1(-h t)
+    float v0, L0, A0;      // base trajectory
+    float2 vb, Lb, Ab;     // bumped pair
+    float T1, Dp, Dm;      // base: sum S t, sum S expm1(h t), sum S expm1(-h t)
 };
 
 __device__ __forceinline__ void traj_step(float& v, float& L, float z1l, float sz2, float ck,
@@ -290,17 +363,33 @@ __device__ __forceinline__ void traj_step(float& v, float& L, float z1l, float s
     v = fmaxf(fmaf(s, sz2, fmaf(v, a.f_omkdt, ck)), 0.0f);
 }
 
-template <bool GREEKS>
-__device__ __forceinline__ void advance(PathState32& st, float z1l, float sz2, const KernelArgs& a) {
-    const float ck = fmaf(sz2 * sz2, a.f_cmil2, a.f_ck0);
-    traj_step(st.v0, st.L0, z1l, sz2, ck, a);
-    if (GREEKS) {
-        traj_step(st.vu, st.Lu, z1l, sz2, ck, a);
-        traj_step(st.vd, st.Ld, z1l, sz2, ck, a);
+// traj_step on the bumped pair, operation for operation; PAIR issues it as
+// paired FFMA2 (bit-identical).  Measured (tools/kernel_variants.py, 2^24 x
+// 252): European 8.44 -> 8.20 ms, RQMC Sobol Asian 3.98 -> 3.93 ms; the
+// MUFU-bound daily-fixing pseudo-random Asian loses 0.3 % and keeps scalar.
+template <bool PAIR>
+__device__ __forceinline__ void traj_step2(float2& v, float2& L, float z1l, float sz2, float ck,
+                                           const KernelArgs& a) {
+    if (PAIR) {
+    const float2 s = make_float2(sqrt_var(v.x), sqrt_var(v.y));
+    L = __ffma2_rn(s, f2(z1l), L);
+    L = __ffma2_rn(v, f2(a.f_nhdt2), L);
+    const float2 t = __ffma2_rn(s, f2(sz2), __ffma2_rn(v, f2(a.f_omkdt), f2(ck)));
+    v = make_float2(fmaxf(t.x, 0.0f), fmaxf(t.y, 0.0f));
+    } else {
+    traj_step(v.x, L.x, z1l, sz2, ck, a);
+    traj_step(v.y, L.y, z1l, sz2, ck, a);
     }
 }
 
-template <bool GREEKS>
+template <bool GREEKS, bool PAIR>
+__device__ __forceinline__ void advance(PathState32& st, float z1l, float sz2, const KernelArgs& a) {
+    const float ck = fmaf(sz2 * sz2, a.f_cmil2, a.f_ck0);
+    traj_step(st.v0, st.L0, z1l, sz2, ck, a);
+    if (GREEKS) traj_step2<PAIR>(st.vb, st.Lb, z1l, sz2, ck, a);
+}
+
+template <bool GREEKS, bool PAIR = false>
 __device__ __forceinline__ void fixing(PathState32& st, const float4 w) {
     const float P = ex2_sel<(HMC_EX2_POLY >= 3)>(st.L0);
     st.A0 = fmaf(P, w.x, st.A0);
@@ -312,7 +401,7 @@ __device__ __forceinline__ void fixing(PathState32& st, const float4 w) {
         // the v0-bumped log-prices stay within |d| << 1 of the base one, so
         // 2^{L+d} = 2^L (1 + d ln2 + (d ln2)^2/2 + (d ln2)^3/6) (rel. err
         // < 6e-8 for |d| <= 0.05); a warp with any larger d uses MUFU.EX2
-        const float du = st.Lu - st.L0, dd = st.Ld - st.L0;
+        const float du = st.Lb.x - st.L0, dd = st.Lb.y - st.L0;
         float Pu, Pd;
         if (__all_sync(0xffffffffu, fmaxf(fabsf(du), fabsf(dd)) <= 0.05f)) {
             auto e2 = [](float d) {
@@ -322,30 +411,39 @@ __device__ __forceinline__ void fixing(PathState32& st, const float4 w) {
             Pu = P * e2(du);
             Pd = P * e2(dd);
         } else {
-            Pu = ex2a(st.Lu);
-            Pd = ex2a(st.Ld);
+            Pu = ex2a(st.Lb.x);
+            Pd = ex2a(st.Lb.y);
         }
-        st.Au = fmaf(Pu, w.x, st.Au);
-        st.Ad = fmaf(Pd, w.x, st.Ad);
+        st.Ab = __ffma2_rn(make_float2(Pu, Pd), f2(w.x), st.Ab);
 #else
         // (carrying Au - A0 instead -- one more FADD per trajectory and
         // fixing -- shrinks Vega's fp32 error ~40x but costs 4 % of the
         // daily-fixing kernel: 10.66 -> 11.08 ms; not taken)
-        st.Au = fmaf(ex2_sel<(HMC_EX2_POLY >= 1)>(st.Lu), w.x, st.Au);
-        st.Ad = fmaf(ex2_sel<(HMC_EX2_POLY >= 2)>(st.Ld), w.x, st.Ad);
+#if HMC_EX2_PAIR_POLY
+        st.Ab = __ffma2_rn(ex2_poly2(st.Lb), f2(w.x), st.Ab);
+#else
+        if (PAIR) {
+            st.Ab = __ffma2_rn(make_float2(ex2_sel<(HMC_EX2_POLY >= 1)>(st.Lb.x),
+                                           ex2_sel<(HMC_EX2_POLY >= 2)>(st.Lb.y)), f2(w.x), st.Ab);
+        } else {
+            st.Ab.x = fmaf(ex2_sel<(HMC_EX2_POLY >= 1)>(st.Lb.x), w.x, st.Ab.x);
+            st.Ab.y = fmaf(ex2_sel<(HMC_EX2_POLY >= 2)>(st.Lb.y), w.x, st.Ab.y);
+        }
+#endif
 #endif
     }
 }
 
-template <int FIX, bool GREEKS>
+// PAIR: the bumped trajectories as paired FFMA2 (see traj_step2)
+template <int FIX, bool GREEKS, bool PAIR = false>
 __device__ __forceinline__ void step(PathState32& st, int k, float z1l, float sz2,
                                      const KernelArgs& a) {
-    advance<GREEKS>(st, z1l, sz2, a);
+    advance<GREEKS, PAIR>(st, z1l, sz2, a);
     if (FIX == kFixEvery) {
-        fixing<GREEKS>(st, __ldg(a.steps32 + k));
+        fixing<GREEKS, PAIR>(st, __ldg(a.steps32 + k));
     } else if (FIX == kFixTable) {
         const float4 w = __ldg(a.steps32 + k);
-        if (w.x != 0.0f) fixing<GREEKS>(st, w);
+        if (w.x != 0.0f) fixing<GREEKS, PAIR>(st, w);
     }
 }
 

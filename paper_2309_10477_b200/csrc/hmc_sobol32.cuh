@@ -13,38 +13,43 @@ namespace hmc {
 // Sobol QMC driver (engine.py:97-101: run r uses points 1 + r*N + path).
 //
 // gray(n) = gray(n & ~31) ^ gray(n & 31) (no carries between the parts), so
-// the XOR of direction numbers splits into a warp-uniform high part U (the
-// warp's <= 2 aligned 32-point blocks) and a lane part T indexed by the
-// lane's 5-bit Gray code.  Both are rebuilt in shared memory for every
-// 64-step chunk of dimensions; the per-step cost is two LDS.64 + two XORs
-// instead of a 30-bit XOR per coordinate.  Optional random digital shift
-// (a.sobol_shift) per (run, dimension) for randomised QMC.
+// the XOR of direction numbers splits into a high part U, shared by the 32
+// points of an aligned 32-point block, and a lane part T indexed by the
+// lane's 5-bit Gray code.  A thread block's consecutive points span at most
+// WARPS + 1 aligned blocks; the refill builds T and those U rows in shared
+// memory for every chunk of STEPS steps (2 STEPS dimensions): the first row
+// from the direction numbers, each next row by XORing the (two) direction
+// numbers in which consecutive blocks' Gray codes differ.  Per step a lane
+// then does two LDS.64 + two XORs.  Optional random digital shift
+// (a.sobol_shift) per (run, dimension) for randomised QMC, folded into U.
 // ---------------------------------------------------------------------------
 constexpr int kSobolSteps = 64;  // steps per table refill (128 dimensions)
 
 template <int STEPS, int WARPS>
 struct SobolTablesT {
     static constexpr int kSteps = STEPS;
-    uint2 T[STEPS][32];          // lane parts, (dim 2q, dim 2q+1)
-    uint2 U[WARPS][2][STEPS];    // per warp: blocks B1, B2
+    static constexpr int kRows = WARPS + 1;
+    uint2 T[STEPS][32];      // lane parts, (dim 2q, dim 2q+1)
+    uint2 U[kRows][STEPS];   // high parts of the block's aligned 32-point blocks
 };
 
 // Gray-code split of this thread's point index (see above)
 struct SobolLane {
-    uint32_t gB1, gB2;  // Gray codes of the warp's two aligned 32-point blocks
-    int which;          // this lane's block
+    uint32_t B0;        // first aligned 32-point block of the thread block
+    int row;            // this lane's block, relative to B0
     uint32_t jl;        // Gray code of the lane part
     unsigned long long key_run;
     float hx, ht;       // half 2^-29, half 2^-30 (half = 0.5: cell midpoints of shifted points)
 
-    __device__ __forceinline__ SobolLane(int run, long long p, const KernelArgs& a) {
+    // p: this thread's path; p_first: the thread block's first path (its
+    // paths are consecutive; a dead lane's row is clamped, its values unused)
+    __device__ __forceinline__ SobolLane(int run, long long p, long long p_first, int max_row,
+                                         const KernelArgs& a) {
         // scrambled (randomised QMC): every run re-uses points 1..N under its own shifts
-        const uint32_t n = (uint32_t)(1 + (a.sobol_scramble ? 0LL : (long long)run * a.n_paths) + p);
-        const uint32_t n0 = __shfl_sync(0xffffffffu, n, 0);
-        const uint32_t B1 = n0 & ~31u;
-        gB1 = B1 ^ (B1 >> 1);
-        gB2 = (B1 + 32) ^ ((B1 + 32) >> 1);
-        which = ((n & ~31u) != B1) ? 1 : 0;
+        const long long off = 1 + (a.sobol_scramble ? 0LL : (long long)run * a.n_paths);
+        const uint32_t n = (uint32_t)(off + p);
+        B0 = (uint32_t)(off + p_first) & ~31u;
+        row = (int)min(max(((long long)(n & ~31u) - (long long)B0) >> 5, 0LL), (long long)max_row);
         const uint32_t c = n & 31u;
         jl = c ^ (c >> 1);
         key_run = derive(a.root_key, (unsigned long long)run);
@@ -58,13 +63,13 @@ struct SobolLane {
 template <class Tab>
 __device__ __forceinline__ void sobol_refill(Tab& tab, int q0, int m, const SobolLane& sl,
                                              const KernelArgs& a) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t* __restrict__ V = a.sobol_v;
     const int dim = a.sobol_dim;
     const int d0 = 2 * q0;
+    const int nd = 2 * m;
     __syncthreads();  // previous chunk fully consumed
     // lane-part table: thread t owns dimension d0 + t, all 32 Gray codes
-    if (threadIdx.x < 2 * m) {
+    if (threadIdx.x < nd) {
         const int d = d0 + threadIdx.x;
         uint32_t v[5];
 #pragma unroll
@@ -77,18 +82,30 @@ __device__ __forceinline__ void sobol_refill(Tab& tab, int q0, int m, const Sobo
 #pragma unroll
         for (int j = 0; j < 32; ++j) col[2 * j] = x[j];
     }
-    // warp-uniform parts for this warp's two aligned blocks
-    for (int dd = lane; dd < 2 * m; dd += 32) {
+    // high parts: (dimension, group of rows) per thread; a group's first row
+    // from the direction numbers, the others incrementally
+    const int groups = max(1, (int)blockDim.x / nd);
+    const int rows_per = (Tab::kRows + groups - 1) / groups;
+    if (threadIdx.x < nd * groups) {
+        const int dd = threadIdx.x % nd, r0 = (threadIdx.x / nd) * rows_per;
+        const int r1 = min(r0 + rows_per, Tab::kRows);
         const int d = d0 + dd;
-        uint32_t u1 = 0, u2d = 0;
-        for (int b = 4; b < kSobolBits; ++b) {
-            const uint32_t vb = ((sl.gB1 | (sl.gB1 ^ sl.gB2)) >> b) & 1u ? __ldg(V + b * dim + d) : 0u;
-            if ((sl.gB1 >> b) & 1u) u1 ^= vb;
-            if (((sl.gB1 ^ sl.gB2) >> b) & 1u) u2d ^= vb;
+        uint32_t B = sl.B0 + 32u * (uint32_t)r0;
+        uint32_t g = B ^ (B >> 1);
+        uint32_t u = 0;
+        for (uint32_t bits = g & ~15u; bits; bits &= bits - 1) u ^= __ldg(V + (__ffs(bits) - 1) * dim + d);
+        const uint32_t sh = a.sobol_scramble ? sobol_shift(sl.key_run, d) : 0u;
+        uint32_t* out = reinterpret_cast<uint32_t*>(&tab.U[0][0]) + (dd >> 1) * 2 + (dd & 1);
+        for (int r = r0; r < r1; ++r) {
+            if (r > r0) {
+                B += 32u;
+                const uint32_t g2 = B ^ (B >> 1);
+                for (uint32_t bits = g ^ g2; bits; bits &= bits - 1)
+                    u ^= __ldg(V + (__ffs(bits) - 1) * dim + d);
+                g = g2;
+            }
+            out[r * 2 * Tab::kSteps] = u ^ sh;
         }
-        if (a.sobol_scramble) u1 ^= sobol_shift(sl.key_run, d);
-        reinterpret_cast<uint32_t*>(&tab.U[warp][0][dd >> 1])[dd & 1] = u1;
-        reinterpret_cast<uint32_t*>(&tab.U[warp][1][dd >> 1])[dd & 1] = u1 ^ u2d;
     }
     __syncthreads();
 }
@@ -98,9 +115,15 @@ template <class Tab>
 __device__ __forceinline__ void sobol_pair(const Tab& tab, int q, const SobolLane& sl,
                                            float& za, float& zb) {
     const uint2 t = tab.T[q][sl.jl];
-    const uint2 u = tab.U[threadIdx.x >> 5][sl.which][q];
+    const uint2 u = tab.U[sl.row][q];
+#if HMC_SOBOL_PAIR
+    const float2 z = sobol_normal_u2(t.x ^ u.x, t.y ^ u.y, sl.hx, sl.ht);
+    za = z.x;
+    zb = z.y;
+#else
     za = sobol_normal_u(t.x ^ u.x, sl.hx, sl.ht);
     zb = sobol_normal_u(t.y ^ u.y, sl.hx, sl.ht);
+#endif
 }
 
 

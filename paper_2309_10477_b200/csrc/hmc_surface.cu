@@ -125,19 +125,19 @@ __device__ __forceinline__ void surface_checkpoint(const PathState32& st, const 
         // European: S_T of each trajectory; r bumps by e^{+-h T}, for which
         // d+ Rp - d- Rm = 0 exactly (the FD numerator is -K (d+ - d-))
         const float Ae = E * ex2a(st.L0);
-        surface_update(hist, g_euro, nb, sK, pow2, s.nK, s, mc.d, Ae, E * ex2a(st.Lu), E * ex2a(st.Ld),
+        surface_update(hist, g_euro, nb, sK, pow2, s.nK, s, mc.d, Ae, E * ex2a(st.Lb.x), E * ex2a(st.Lb.y),
                        Ae * mc.ehp, Ae * mc.ehm, 0.0f, 0.0f);
         // Asian: average of S over grid dates t_1..t_m;
         // a = [A (d+ - d-) + (d+ D+ - d- D-)/N] / 2h_r, both terms same sign
         const float inv = mc.inv_n;
         const float Aa = st.A0 * inv;
         const float al = (Aa * mc.ddisc + (mc.dp * st.Dp - mc.dm * st.Dm) * inv) * s.inv_2hr;
-        surface_update(hist + per_style, g_asian, nb, sK, pow2, s.nK, s, mc.d, Aa, st.Au * inv, st.Ad * inv,
+        surface_update(hist + per_style, g_asian, nb, sK, pow2, s.nK, s, mc.d, Aa, st.Ab.x * inv, st.Ab.y * inv,
                        fmaf(st.Dp, inv, Aa), fmaf(st.Dm, inv, Aa), fmaf(st.T1, inv, -mc.T * Aa), al);
     }
 #else
     // keep the path computation alive in the timing experiment
-    if (st.A0 + st.Au + st.Ad + st.L0 + st.Lu + st.Ld + st.T1 + st.Dp + st.Dm == 1.2345e-30f) atomicAdd(hist, 1);
+    if (st.A0 + st.Ab.x + st.Ab.y + st.L0 + st.Lb.x + st.Lb.y + st.T1 + st.Dp + st.Dm == 1.2345e-30f) atomicAdd(hist, 1);
 #endif
     __syncthreads();
 #ifdef HMC_SURF_EXP_NOFLUSH
@@ -186,17 +186,16 @@ __global__ void __launch_bounds__(kSurfThreads, kSurfMinBlocks) surface_kernel(c
         const uint32_t c1 = (uint32_t)(live ? path : a.path_lo);
         PathState32 st;
         st.v0 = a.f_v0;
-        st.vu = a.f_vu;
-        st.vd = a.f_vd;
-        st.L0 = st.Lu = st.Ld = 0.0f;
-        st.A0 = st.Au = st.Ad = 0.0f;
+        st.vb = make_float2(a.f_vu, a.f_vd);
+        st.L0 = st.A0 = 0.0f;
+        st.Lb = st.Ab = make_float2(0.0f, 0.0f);
         st.T1 = st.Dp = st.Dm = 0.0f;
         int m = 0, next = s.mats[0].step;
         if (SAMPLER == HMC_SAMPLER_SOBOL) {
             // the single-product Sobol driver's points and quantile (same
             // dimensions 2(k-1), 2(k-1)+1 per step), checkpoints in between
             __shared__ SurfSobolTables tab;
-            const SobolLane sl(run, live ? path : a.path_lo, a);
+            const SobolLane sl(run, path, a.path_lo + tile * kSurfThreads, kSurfThreads / 32, a);
             const float c1 = kSqrt2f * a.f_sqdt * a.f_log2e, cs = kSqrt2f * a.f_sigma * a.f_sqdt;
 #pragma unroll 1
             for (int k0 = 1; k0 <= a.n_sim; k0 += kSurfSobolSteps) {
@@ -207,7 +206,7 @@ __global__ void __launch_bounds__(kSurfThreads, kSurfMinBlocks) surface_kernel(c
                     const int k = k0 + q;
                     float za, zb;
                     sobol_pair(tab, q, sl, za, zb);
-                    step<kFixEvery, true>(st, k, c1 * za, cs * fmaf(a.f_rho, za, a.f_sq1mr2 * zb), a);
+                    step<kFixEvery, true, true>(st, k, c1 * za, cs * fmaf(a.f_rho, za, a.f_sq1mr2 * zb), a);
                     if (k == next) {
                         surface_checkpoint(st, a, s, m, live, hist, sK, pow2, gacc);
                         ++m;

@@ -20,10 +20,7 @@ VDIR = os.path.join(ROOT, "paper_2309_10477_b200", "_variants")
 
 VARIANTS = {
     "base": {},
-    "lb6": {"HMC_MIN_BLOCKS": 6},
     "lb8": {"HMC_MIN_BLOCKS": 8},
-    "lb10": {"HMC_MIN_BLOCKS": 10},
-    "lb12": {"HMC_MIN_BLOCKS": 12},
 }
 
 
