@@ -110,20 +110,31 @@ __device__ __forceinline__ void sobol_refill(Tab& tab, int q0, int m, const Sobo
     __syncthreads();
 }
 
+// the two 30-bit coordinates of pair q of the loaded chunk
+template <class Tab>
+__device__ __forceinline__ uint2 sobol_coords(const Tab& tab, int q, const SobolLane& sl) {
+    const uint2 t = tab.T[q][sl.jl];
+    const uint2 u = tab.U[sl.row][q];
+    return make_uint2(t.x ^ u.x, t.y ^ u.y);
+}
+
+// the two standard normals (divided by sqrt(2)) of a coordinate pair
+__device__ __forceinline__ void sobol_normals(uint2 x, const SobolLane& sl, float& za, float& zb) {
+#if HMC_SOBOL_PAIR
+    const float2 z = sobol_normal_u2(x.x, x.y, sl.hx, sl.ht);
+    za = z.x;
+    zb = z.y;
+#else
+    za = sobol_normal_u(x.x, sl.hx, sl.ht);
+    zb = sobol_normal_u(x.y, sl.hx, sl.ht);
+#endif
+}
+
 // the two standard normals (divided by sqrt(2)) of pair q of the loaded chunk
 template <class Tab>
 __device__ __forceinline__ void sobol_pair(const Tab& tab, int q, const SobolLane& sl,
                                            float& za, float& zb) {
-    const uint2 t = tab.T[q][sl.jl];
-    const uint2 u = tab.U[sl.row][q];
-#if HMC_SOBOL_PAIR
-    const float2 z = sobol_normal_u2(t.x ^ u.x, t.y ^ u.y, sl.hx, sl.ht);
-    za = z.x;
-    zb = z.y;
-#else
-    za = sobol_normal_u(t.x ^ u.x, sl.hx, sl.ht);
-    zb = sobol_normal_u(t.y ^ u.y, sl.hx, sl.ht);
-#endif
+    sobol_normals(sobol_coords(tab, q, sl), sl, za, zb);
 }
 
 
