@@ -416,7 +416,21 @@ def run_b200(args) -> None:
         dist.destroy_process_group()
 
 
+def _claim_stdout():
+    """Keep stdout for the one JSON line: NCCL prints its version banner to
+    file descriptor 1 at communicator creation, so under torch.distributed.run
+    fd 1 is pointed at stderr and the JSON goes to a private dup of the
+    original stdout."""
+    if "LOCAL_RANK" not in os.environ:
+        return
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    sys.stdout = os.fdopen(saved, "w", buffering=1)
+
+
 def main():
+    _claim_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)

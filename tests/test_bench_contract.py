@@ -50,3 +50,15 @@ def test_b200_arm_fails_loudly_without_gpu():
     r = _run(["--steps", "1", "--warmup", "3"])
     assert r.returncode != 0
     assert '"value"' not in r.stdout
+
+
+@pytest.mark.skipif(oracle.ref_core() is None, reason="oracle/_ref (reference kernel) not built")
+def test_json_line_owns_stdout_under_torchrun():
+    """Under torch.distributed.run (LOCAL_RANK set) file descriptor 1 is
+    handed to stderr, so banners written straight to fd 1 (NCCL prints its
+    version there) cannot precede the JSON line."""
+    r = _run(["--impl", "reference", "--steps", "1", "--warmup", "0"], HMC_BENCH_REF_PATHS="4096",
+             LOCAL_RANK="0", RANK="0", WORLD_SIZE="1")
+    assert r.returncode == 0, r.stderr[-2000:]
+    out = r.stdout.splitlines()
+    assert len(out) == 1 and json.loads(out[0])["impl"] == "reference"

@@ -20,9 +20,7 @@ VDIR = os.path.join(ROOT, "paper_2309_10477_b200", "_variants")
 
 VARIANTS = {
     "base": {},
-    "prefetch": {"HMC_SOBOL_PREFETCH": 1},
-    "lb10": {"HMC_MIN_BLOCKS": 10},
-    "prefetch_lb10": {"HMC_SOBOL_PREFETCH": 1, "HMC_MIN_BLOCKS": 10},
+    "ex2pair": {"HMC_EX2_PAIR_POLY": 1},
 }
 
 
