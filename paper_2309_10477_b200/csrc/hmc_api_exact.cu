@@ -59,7 +59,7 @@ int hmc_exact_runs_f64(const hmc_model* model, double s0, const double* step_tim
     int dev = 0, sms = 148;
     HMC_CK(cudaGetDevice(&dev));
     HMC_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    int grid = 0, variant = 4;
+    int grid = 0, variant = 1;
     HMC_CK(hmc::exact_plan(rows, sms, &grid, &variant));
     const size_t threads = (size_t)grid * hmc::kExactThreads;
     cudaStream_t st;
@@ -199,7 +199,7 @@ int hmc_exact_greeks_chunks(const hmc_model* model, const hmc_product* product, 
     // within ~2 GB of device memory
     const long long per_run = n * 3 * (long long)sizeof(double) * n_var;
     const long long batch = std::max(1LL, std::min(R, (2LL << 30) / std::max(per_run, 1LL)));
-    int grid = 0, variant = 4;
+    int grid = 0, variant = 1;
     HMC_CK(hmc::exact_plan(n * batch, sms, &grid, &variant));
     const long long n_tiles = n_tiles_of(n), n_chunks = n_chunks_of(n);
     const size_t tb = ((size_t)n_steps + 1) * sizeof(double), fb = (size_t)n_steps * sizeof(long long);

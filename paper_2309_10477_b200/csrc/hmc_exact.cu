@@ -26,6 +26,15 @@
 
 namespace hmc {
 
+#ifndef HMC_EXACT_NOINLINE
+#define HMC_EXACT_NOINLINE 1
+#endif
+#if HMC_EXACT_NOINLINE
+#define HMC_EXACT_FN __device__ __noinline__
+#else
+#define HMC_EXACT_FN __device__
+#endif
+
 namespace {
 
 constexpr int kMaxNodes = 20000;
@@ -78,7 +87,7 @@ enum { kErrNone = 0, kErrBesselRange = 1, kErrBesselConv = 2, kErrQuad = 3, kErr
 
 // power series of the modified Bessel function I_nu(z) / ((z/2)^nu / Gamma(nu+1))
 // (_core.pyx:143-159)
-__device__ cplx bessel_series(double nu, cplx z, int* err) {
+HMC_EXACT_FN cplx bessel_series(double nu, cplx z, int* err) {
     if (cabs_(z) > 50.0) {
         *err = kErrBesselRange;
         return cx(0.0);
@@ -95,7 +104,7 @@ __device__ cplx bessel_series(double nu, cplx z, int* err) {
 }
 
 // conditional characteristic function of the integrated variance (_core.pyx:162-188)
-__device__ cplx phi_eval(double kappa, double sigma2, double nu, double v_u, double v_t, double tau,
+HMC_EXACT_FN cplx phi_eval(double kappa, double sigma2, double nu, double v_u, double v_t, double tau,
                          double a, int* err) {
     if (a == 0.0) return cx(1.0);
     const cplx g = csqrt_(cx(kappa * kappa, -2.0 * sigma2 * a));
@@ -118,7 +127,7 @@ __device__ cplx phi_eval(double kappa, double sigma2, double nu, double v_u, dou
     return lead * expo * ratio;
 }
 
-__device__ double ndtri_d(double u) {
+HMC_EXACT_FN double ndtri_d(double u) {
     double q, s, num, den, x, e, corr, p, sign;
     if (u < 1e-300) u = 1e-300;
     if (u > 1.0 - 1e-16) u = 1.0 - 1e-16;
@@ -152,7 +161,7 @@ __device__ double ndtri_d(double u) {
 }
 
 // Marsaglia-Tsang on the reference stream (_core.pyx:116-136)
-__device__ double sample_gamma(unsigned long long key, double shape, double scale) {
+HMC_EXACT_FN double sample_gamma(unsigned long long key, double shape, double scale) {
     double boost = 1.0, alpha = shape;
     unsigned long long ctr = 0;
     if (alpha < 1.0) {
@@ -192,7 +201,7 @@ __device__ double cdf_at(double x, double h, int n, const NodeCache& nc, int* er
     return f;
 }
 
-__device__ double bisect_iv(double u, double lo, double hi, double h, int n, const NodeCache& nc,
+HMC_EXACT_FN double bisect_iv(double u, double lo, double hi, double h, int n, const NodeCache& nc,
                             int* err) {
     const double f_hi = cdf_at(hi, h, n, nc, err);
     if (f_hi < u - kNewtonTol) {
@@ -320,11 +329,15 @@ __device__ double sample_iv(double kappa, double theta, double sigma, double dof
 
 }  // namespace
 
-// Two register budgets (tools/exact_prof.py, European, one step):
-// MINB = 3 blocks/SM (158 regs) is fastest for deep grid-stride loops
-// (2^20 paths: 30.0 ms vs 35.0 ms at 4 blocks / 128 regs, 33.5 ms at 2 blocks
-// / 184 regs; 5-8 blocks spill, 38-43 ms), MINB = 4 for jobs of a few waves
-// (2^17 paths: 2.35 ms vs 2.88 ms) -- exact_plan picks per launch.
+// Two register budgets, picked per launch by exact_plan: a wide one for jobs
+// of a few waves and a deep one for long grid-stride loops.  The series,
+// characteristic-function, Gamma and bisection routines are out-of-line
+// calls (HMC_EXACT_NOINLINE): inlined at every call site the kernel was
+// 431 KB of SASS and stalled on instruction fetch; out of line it is 136 KB
+// and 2^20 paths run in 28.6 instead of 33.1 ms (tools/exact_prof.py).  With
+// call frames on the stack, higher occupancy then pays a little: 8 / 6
+// blocks per SM (64 / 80 registers) against the inlined kernel's 4 / 3
+// (128 / 158): 2^17 paths 4.3 ms, 2^20 26-28 ms (noise +-5 %).
 template <int MINB>
 __global__ void __launch_bounds__(kExactThreads, MINB) exact_batch_kernel(const ExactArgs e) {
     const long long n = e.path_hi - e.path_lo;
@@ -461,16 +474,27 @@ cudaError_t launch_exact_estimators(const KernelArgs& a, const double* const obs
     return cudaGetLastError();
 }
 
+#ifndef HMC_EXACT_MINB_WIDE
+#define HMC_EXACT_MINB_WIDE 8
+#endif
+#ifndef HMC_EXACT_MINB_DEEP
+#define HMC_EXACT_MINB_DEEP 6
+#endif
+constexpr int kMinBWide = HMC_EXACT_MINB_WIDE, kMinBDeep = HMC_EXACT_MINB_DEEP;
+
+// variant 1: the wide budget (jobs of a few waves), 0: the deep one
 cudaError_t exact_plan(long long rows, int sms, int* grid, int* variant) {
     int occ_wide = 0, occ_deep = 0;
-    cudaError_t err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_wide, exact_batch_kernel<4>,
+    cudaError_t err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_wide, exact_batch_kernel<kMinBWide>,
                                                                     kExactThreads, 0);
     if (err == cudaSuccess)
-        err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_deep, exact_batch_kernel<3>, kExactThreads, 0);
+        err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_deep, exact_batch_kernel<kMinBDeep>,
+                                                            kExactThreads, 0);
     if (err != cudaSuccess) return err;
-    const long long wave = (long long)sms * (occ_wide > 0 ? occ_wide : 4) * kExactThreads;
-    *variant = rows > 4 * wave ? 3 : 4;  // deep loops: fewer, fatter threads
-    const long long per_sm = *variant == 3 ? (occ_deep > 0 ? occ_deep : 3) : (occ_wide > 0 ? occ_wide : 4);
+    const long long wave = (long long)sms * (occ_wide > 0 ? occ_wide : kMinBWide) * kExactThreads;
+    *variant = rows > 4 * wave ? 0 : 1;  // deep loops: fewer, fatter threads
+    const long long per_sm = *variant == 0 ? (occ_deep > 0 ? occ_deep : kMinBDeep)
+                                           : (occ_wide > 0 ? occ_wide : kMinBWide);
     const long long blocks = (rows + kExactThreads - 1) / kExactThreads;
     const long long max_blocks = (long long)sms * per_sm;  // grid-stride: one resident wave
     *grid = (int)(blocks < max_blocks ? blocks : max_blocks);
@@ -478,10 +502,10 @@ cudaError_t exact_plan(long long rows, int sms, int* grid, int* variant) {
 }
 
 cudaError_t launch_exact(const ExactArgs& e, int grid, int variant, cudaStream_t s) {
-    if (variant == 3)
-        exact_batch_kernel<3><<<grid, kExactThreads, 0, s>>>(e);
+    if (variant == 0)
+        exact_batch_kernel<kMinBDeep><<<grid, kExactThreads, 0, s>>>(e);
     else
-        exact_batch_kernel<4><<<grid, kExactThreads, 0, s>>>(e);
+        exact_batch_kernel<kMinBWide><<<grid, kExactThreads, 0, s>>>(e);
     return cudaGetLastError();
 }
 
