@@ -19,6 +19,7 @@ VDIR = os.path.join(ROOT, "paper_2309_10477_b200", "_variants")
 
 VARIANTS = {
     "s1024x1": {},
+    "noinline": {"HMC_SURF_NOINLINE": 1},
     "s512x2": {"HMC_SURF_THREADS": 512, "HMC_SURF_MINB": 2},
     "s256x4": {"HMC_SURF_THREADS": 256, "HMC_SURF_MINB": 4},
     "s768x1": {"HMC_SURF_THREADS": 768, "HMC_SURF_MINB": 1},
