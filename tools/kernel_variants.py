@@ -20,10 +20,7 @@ VDIR = os.path.join(ROOT, "paper_2309_10477_b200", "_variants")
 
 VARIANTS = {
     "base": {},
-    "w8d6": {"HMC_EXACT_MINB_WIDE": 8, "HMC_EXACT_MINB_DEEP": 6},
-    "w8d8": {"HMC_EXACT_MINB_WIDE": 8, "HMC_EXACT_MINB_DEEP": 8},
-    "w10d10": {"HMC_EXACT_MINB_WIDE": 10, "HMC_EXACT_MINB_DEEP": 10},
-    "w12d12": {"HMC_EXACT_MINB_WIDE": 12, "HMC_EXACT_MINB_DEEP": 12},
+    "x_noweights": {"HMC_EXP_NO_WEIGHT_LOAD": 1},
 }
 
 
