@@ -36,8 +36,13 @@ def test_plain_c_host(tmp_path):
     assert rows["put_greeks_rc"][0] == "-4"
 
 
-@pytest.mark.parametrize("n_paths,n_runs,n_dev", [(70001, 3, 3), (40000, 2, 7), (2**20, 1, 2)])
-def test_greeks_multi_bit_identical(n_paths, n_runs, n_dev):
+@pytest.mark.parametrize("n_paths,n_runs,n_dev,qmc", [
+    (70001, 3, 3, {}), (40000, 2, 7, {}), (2**20, 1, 2, {}),
+    # Sobol: slices start at chunk boundaries, runs at 1 + r N (unaligned
+    # 32-point blocks for the Gray-code tables), or every run at point 1
+    (70001, 3, 3, dict(sampler="sobol", sobol_highdim_ack=True)),
+    (40000, 2, 3, dict(sampler="sobol", sobol_highdim_ack=True, sobol_scramble=True))])
+def test_greeks_multi_bit_identical(n_paths, n_runs, n_dev, qmc):
     """hmc_greeks_multi deals chunk-aligned slices over a device list (here
     the one GPU repeated: separate streams and buffers, the same code path
     as distinct GPUs) and must reproduce hmc_greeks bit for bit, including
@@ -48,7 +53,11 @@ def test_greeks_multi_bit_identical(n_paths, n_runs, n_dev):
     p = HestonParams(**BENCH_PARAMS)
     spec = OptionSpec("asian_arithmetic", "call", 100.0, 1.0, 100.0, averaging_times=daily_fixings(1.0, 64))
     job = engine.Job(p, spec, SimConfig(scheme="milstein", n_paths=n_paths, n_steps=64, n_runs=n_runs,
-                                        seed=5), True)
+                                        seed=5, **qmc), True)
+    if job.sobol_host is not None:       # host direction numbers for the one-call entries
+        v = np.ascontiguousarray(job.sobol_host)
+        job.sim.sobol_v = v.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))
+        job.sim.sobol_v_on_device = 0
     L = _lib.lib()
     one = np.zeros((n_runs, _lib.HMC_NW))
     multi = np.zeros((n_runs, _lib.HMC_NW))
@@ -81,3 +90,4 @@ def test_integration_md_ctypes_stub_runs():
     ref = cuda_backend.discretised_batch(p, 100.0, 1.0, 32, True, 0, 256, 12345, None, avg)
     assert ns["BACKEND_NAME"] == "cuda"
     np.testing.assert_array_equal(got, ref)
+
