@@ -168,11 +168,11 @@ __global__ void HMC_BOUNDS fast_greeks_kernel(const KernelArgs a,
     st.T1 = st.Dp = st.Dm = 0.0f;
 
     if (SAMPLER == HMC_SAMPLER_PSEUDO) {
-        // counter (step pair, path, key_run lo, key_run hi), fixed key
+        // counter (step triple, path, key_run lo, key_run hi), fixed key;
+        // one Philox block feeds three Box-Muller steps (tri_unpack)
         const unsigned long long key_run = derive(a.root_key, (unsigned long long)run);
         const uint32_t c1 = (uint32_t)p;
         const uint32_t c2 = (uint32_t)key_run, c3 = (uint32_t)(key_run >> 32);
-#if HMC_TRIPACK
         const int ntri = a.n_sim / 3;
         int k = 1;
 #pragma unroll 1
@@ -198,34 +198,6 @@ __global__ void HMC_BOUNDS fast_greeks_kernel(const KernelArgs a,
                 step<FIX, GREEKS, FIX == kFixLast>(st, k + i, z1l, sz2, a);
             }
         }
-#else
-        const int npairs = a.n_sim >> 1;
-        int k = 1;
-#if HMC_PIPELINE_RNG
-        uint4 xn = philox4x32_10(0u, c1, c2, c3);
-#endif
-        HMC_UNROLL(HMC_UNROLL_PAIRS)
-        for (int j = 0; j < npairs; ++j) {
-#if HMC_PIPELINE_RNG
-            const uint4 x = xn;
-            xn = philox4x32_10((uint32_t)(j + 1), c1, c2, c3);
-#else
-            const uint4 x = philox4x32_10((uint32_t)j, c1, c2, c3);
-#endif
-            float z1l, sz2;
-            box_muller(x.x, x.y, a, z1l, sz2);
-            step<FIX, GREEKS, FIX == kFixLast>(st, k, z1l, sz2, a);
-            box_muller(x.z, x.w, a, z1l, sz2);
-            step<FIX, GREEKS, FIX == kFixLast>(st, k + 1, z1l, sz2, a);
-            k += 2;
-        }
-        if (a.n_sim & 1) {
-            const uint4 x = philox4x32_10((uint32_t)npairs, c1, c2, c3);
-            float z1l, sz2;
-            box_muller(x.x, x.y, a, z1l, sz2);
-            step<FIX, GREEKS, FIX == kFixLast>(st, k, z1l, sz2, a);
-        }
-#endif
     } else if (SAMPLER == HMC_SAMPLER_SOBOL) {
         sobol_paths<FIX, GREEKS>(st, run, p, a);
     } else {

@@ -23,24 +23,12 @@
 #ifndef HMC_SQRT_RSQ
 #define HMC_SQRT_RSQ 0
 #endif
-#ifndef HMC_PIPELINE_RNG
-#define HMC_PIPELINE_RNG 0   // generate step pair j+1's Philox block during pair j
-#endif
 #ifndef HMC_EX2_DELTA
 #define HMC_EX2_DELTA 0      // bumped trajectories' 2^L from the base one (guarded)
-#endif
-#ifndef HMC_TRIPACK
-#define HMC_TRIPACK 1        // 3 steps per Philox block (23-bit radius, 19/18-bit angle)
 #endif
 #ifndef HMC_EX2_PAIR_POLY
 #define HMC_EX2_PAIR_POLY 0  // bumped pair's 2^L by a paired FMA polynomial instead of 2 MUFU.EX2
 #endif
-#ifndef HMC_UNROLL_PAIRS
-#define HMC_UNROLL_PAIRS 1
-#endif
-#define HMC_PRAGMA_(x) _Pragma(#x)
-#define HMC_UNROLL_(n) HMC_PRAGMA_(unroll n)
-#define HMC_UNROLL(n) HMC_UNROLL_(n)
 
 namespace hmc {
 
@@ -172,40 +160,6 @@ __device__ __forceinline__ void tri_unpack(const uint4 w, float (&fr)[3], float 
     fa[0] = __uint_as_float(((w.w >> 9) & 0x007FFFF0u) | 0x3f800000u);
     fa[1] = __uint_as_float(((w.w << 10) & 0x007FFC00u) | ((w.x << 1) & 0x000003F0u) | 0x3f800000u);
     fa[2] = __uint_as_float(((w.y << 14) & 0x007FC000u) | ((w.z << 5) & 0x00003FE0u) | 0x3f800000u);
-}
-
-__device__ __forceinline__ void box_muller(uint32_t xr, uint32_t xa, const KernelArgs& a,
-                                           float& z1l, float& sz2) {
-    const float u1 = 2.0f - one_to_two(xr);                  // (0, 1]
-    const float R = sqrta(lg2a(u1) * a.f_bm2);               // sqrt(dt) sqrt(-2 ln u1) log2 e
-    float sn, cs;
-#if HMC_SINCOS_POLY
-    // angle in [-pi/2, pi/2) from the top 23 bits, sin/cos by Taylor
-    // polynomials (abs err 6e-8), cos sign from a spare (low) bit of xr
-    const float r = fmaf(one_to_two(xa), 2.0f, -3.0f);       // [-1, 1)
-    const float r2 = r * r;
-    float ps = -3.598843235212084e-06f;
-    ps = fmaf(ps, r2, 1.6044118478735975e-04f);
-    ps = fmaf(ps, r2, -4.681754135318687e-03f);
-    ps = fmaf(ps, r2, 7.969262624616703e-02f);
-    ps = fmaf(ps, r2, -6.459640975062462e-01f);
-    ps = fmaf(ps, r2, 1.5707963267948966f);
-    sn = ps * r;
-    float pc = 4.710874778818169e-07f;
-    pc = fmaf(pc, r2, -2.5202042373060596e-05f);
-    pc = fmaf(pc, r2, 9.192602748394263e-04f);
-    pc = fmaf(pc, r2, -2.0863480763352957e-02f);
-    pc = fmaf(pc, r2, 2.53669507901048e-01f);
-    pc = fmaf(pc, r2, -1.2337005501361697f);
-    pc = fmaf(pc, r2, 1.0f);
-    cs = __uint_as_float(__float_as_uint(pc) ^ (xr << 31));
-#else
-    const float th = fmaf(one_to_two(xa), 6.28318530717958647692f, -9.42477796076937971538f);
-    sn = __sinf(th);                                         // th in [-pi, pi)
-    cs = __cosf(th);
-#endif
-    z1l = R * cs;
-    sz2 = R * fmaf(a.f_cA, cs, a.f_cB * sn);
 }
 
 // Standard-normal quantile of the Sobol coordinate u = (x + half) 2^-30:
