@@ -46,6 +46,7 @@ constexpr int kBisectMaxIter = 200;
 constexpr double kPeriodStds = 12.0;
 constexpr double kDegenerateRelStd = 1e-5;
 constexpr double kPi = 3.14159265358979323846;
+constexpr int kRotSeed = 32;
 
 struct cplx {
     double re, im;
@@ -57,7 +58,10 @@ __device__ __forceinline__ cplx operator*(cplx a, cplx b) {
     return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re};
 }
 __device__ __forceinline__ cplx operator*(double s, cplx a) { return {s * a.re, s * a.im}; }
-__device__ __forceinline__ cplx operator/(cplx a, double s) { return {a.re / s, a.im / s}; }
+__device__ __forceinline__ cplx operator/(cplx a, double s) {
+    const double r = 1.0 / s;  // one division
+    return {a.re * r, a.im * r};
+}
 // Smith's algorithm (robust complex division)
 __device__ __forceinline__ cplx operator/(cplx a, cplx b) {
     if (fabs(b.re) >= fabs(b.im)) {
@@ -67,7 +71,11 @@ __device__ __forceinline__ cplx operator/(cplx a, cplx b) {
     const double r = b.re / b.im, d = b.re * r + b.im;
     return {(a.re * r + a.im) / d, (a.im * r - a.re) / d};
 }
-__device__ __forceinline__ double cabs_(cplx a) { return hypot(a.re, a.im); }
+// |a|: the magnitudes here are moderate (Bessel arguments <= 50, series
+// values <= e^50), so sqrt(re^2 + im^2) cannot over/underflow where hypot's
+// scaling would matter; within an ulp of hypot at a third of the cost
+__device__ __forceinline__ double norm2_(cplx a) { return a.re * a.re + a.im * a.im; }
+__device__ __forceinline__ double cabs_(cplx a) { return sqrt(norm2_(a)); }
 __device__ __forceinline__ cplx cexp_(cplx a) {
     const double e = exp(a.re);
     double s, c;
@@ -97,34 +105,62 @@ HMC_EXACT_FN cplx bessel_series(double nu, cplx z, int* err) {
     for (int k = 1; k <= 400; ++k) {
         term = term * q / (k * (nu + k));
         total = total + term;
-        if (cabs_(term) < 1e-12 * cabs_(total)) return total;
+        // |term| < 1e-12 |total|, compared squared (no square roots)
+        if (norm2_(term) < 1e-24 * norm2_(total)) return total;
     }
     *err = kErrBesselConv;
     return total;
 }
 
-// conditional characteristic function of the integrated variance (_core.pyx:162-188)
-HMC_EXACT_FN cplx phi_eval(double kappa, double sigma2, double nu, double v_u, double v_t, double tau,
-                         double a, int* err) {
-    if (a == 0.0) return cx(1.0);
-    const cplx g = csqrt_(cx(kappa * kappa, -2.0 * sigma2 * a));
-    const double ek = exp(-kappa * tau);
-    const cplx eg = cexp_(cx(-g.re * tau, -g.im * tau));
-    const cplx one = cx(1.0);
-    const cplx lead = (g * cexp_(-0.5 * ((g - cx(kappa)) * cx(tau))) * cx(1.0 - ek)) /
-                      (cx(kappa) * (one - eg));
-    const cplx bracket = cx(kappa * (1.0 + ek) / (1.0 - ek)) - (g * (one + eg)) / (one - eg);
-    const cplx expo = cexp_(((v_u + v_t) / sigma2) * bracket);
-    const cplx egh = cexp_(-0.5 * (g * cx(tau)));
-    const cplx coeff_g = (4.0 * (g * egh)) / (cx(sigma2) * (one - egh * egh));
+// conditional characteristic function of the integrated variance
+// (_core.pyx:162-188), split into the per-path constants (PhiPath: every
+// term that does not depend on the transform variable a, including the
+// denominator Bessel series of real argument) and the per-node part.  The
+// reference re-evaluates all of it at every node; hoisting is bit-identical
+// (same operations on the same inputs) and removes one of the two series.
+struct PhiPath {
+    double kappa, sigma2, nu, tau;
+    double ek, one_m_ek, kb, vs, w, log1m_ek;
+    cplx den;      // bessel_series(nu, w coeff_k)
+    int den_err;   // its error code (kErrNone = 0)
+};
+
+HMC_EXACT_FN PhiPath phi_path(double kappa, double sigma2, double nu, double v_u, double v_t, double tau) {
+    PhiPath P;
+    P.kappa = kappa;
+    P.sigma2 = sigma2;
+    P.nu = nu;
+    P.tau = tau;
+    P.ek = exp(-kappa * tau);
+    P.one_m_ek = 1.0 - P.ek;
+    P.kb = kappa * (1.0 + P.ek) / (1.0 - P.ek);
+    P.vs = (v_u + v_t) / sigma2;
     const double ekh = exp(-0.5 * kappa * tau);
     const double coeff_k = 4.0 * kappa * ekh / (sigma2 * (1.0 - ekh * ekh));
-    const double w = sqrt(v_u * v_t);
-    const cplx log_q = clog_(g / kappa) - 0.5 * ((g - cx(kappa)) * cx(tau)) + cx(log(1.0 - ek)) -
+    P.w = sqrt(v_u * v_t);
+    P.log1m_ek = log(1.0 - P.ek);
+    P.den_err = 0;
+    P.den = bessel_series(nu, cx(P.w * coeff_k), &P.den_err);
+    return P;
+}
+
+HMC_EXACT_FN cplx phi_node(const PhiPath& P, double a, int* err) {
+    if (a == 0.0) return cx(1.0);
+    const double kappa = P.kappa, sigma2 = P.sigma2, nu = P.nu, tau = P.tau;
+    const cplx g = csqrt_(cx(kappa * kappa, -2.0 * sigma2 * a));
+    const cplx eg = cexp_(cx(-g.re * tau, -g.im * tau));
+    const cplx one = cx(1.0);
+    const cplx lead = (g * cexp_(-0.5 * ((g - cx(kappa)) * cx(tau))) * cx(P.one_m_ek)) /
+                      (cx(kappa) * (one - eg));
+    const cplx bracket = cx(P.kb) - (g * (one + eg)) / (one - eg);
+    const cplx expo = cexp_(P.vs * bracket);
+    const cplx egh = cexp_(-0.5 * (g * cx(tau)));
+    const cplx coeff_g = (4.0 * (g * egh)) / (cx(sigma2) * (one - egh * egh));
+    const cplx log_q = clog_(g / kappa) - 0.5 * ((g - cx(kappa)) * cx(tau)) + cx(P.log1m_ek) -
                        clog_(one - eg);
-    const cplx ratio = (cexp_(nu * log_q) * bessel_series(nu, w * coeff_g, err)) /
-                       bessel_series(nu, cx(w * coeff_k), err);
-    return lead * expo * ratio;
+    const cplx num = cexp_(nu * log_q) * bessel_series(nu, P.w * coeff_g, err);
+    if (P.den_err != kErrNone) *err = P.den_err;
+    return lead * expo * (num / P.den);
 }
 
 HMC_EXACT_FN double ndtri_d(double u) {
@@ -188,12 +224,25 @@ struct NodeCache {
     long long stride;
     int cap;
     // for recomputation past the cache
-    double kappa, sigma2, nu, v_u, v_t, tau, h;
+    const PhiPath* P;
+    double h;
     __device__ double re(int j, int* err) const {  // j 0-based
         if (j < cap) return base[(size_t)j * stride];
-        return phi_eval(kappa, sigma2, nu, v_u, v_t, tau, (j + 1) * h, err).re;
+        return phi_node(*P, (j + 1) * h, err).re;
     }
 };
+
+// 1 / j for the Fourier-series weights: a constant-memory table (the loop
+// index is warp-uniform, so the load broadcasts) instead of a division
+constexpr int kInvTable = 512;
+struct InvIntTable {
+    double v[kInvTable];
+    constexpr InvIntTable() : v() {
+        for (int j = 1; j < kInvTable; ++j) v[j] = 1.0 / j;  // IEEE division, as on the device
+    }
+};
+__constant__ InvIntTable c_inv_int = InvIntTable();
+__device__ __forceinline__ double inv_int(int j) { return j < kInvTable ? c_inv_int.v[j] : 1.0 / j; }
 
 __device__ double cdf_at(double x, double h, int n, const NodeCache& nc, int* err) {
     double f = h * x / kPi;
@@ -241,15 +290,16 @@ __device__ double sample_iv(double kappa, double theta, double sigma, double dof
     scale *= dt;
     double m1 = scale, eps;
     cplx phi;
+    const PhiPath P = phi_path(kappa, sigma2, nu, v_u, v_t, dt);
     for (int it = 0; it < 2; ++it) {
         eps = 0.05 / m1;
-        phi = phi_eval(kappa, sigma2, nu, v_u, v_t, dt, eps, err);
+        phi = phi_node(P, eps, err);
         const double m1_new = phi.im / eps;
         if (!(m1_new > 0.0) || !isfinite(m1_new)) break;
         m1 = m1_new;
     }
     eps = 0.05 / m1;
-    phi = phi_eval(kappa, sigma2, nu, v_u, v_t, dt, eps, err);
+    phi = phi_node(P, eps, err);
     m1 = phi.im / eps;
     const double m2 = -2.0 * (phi.re - 1.0) / (eps * eps);
     double var = m2 - m1 * m1;
@@ -261,12 +311,7 @@ __device__ double sample_iv(double kappa, double theta, double sigma, double dof
         return r > 0.0 ? r : 0.0;
     }
     const double h = 2.0 * kPi / (mean + kPeriodStds * std);
-    nc.kappa = kappa;
-    nc.sigma2 = sigma2;
-    nc.nu = nu;
-    nc.v_u = v_u;
-    nc.v_t = v_t;
-    nc.tau = dt;
+    nc.P = &P;
     nc.h = h;
 
     int n = 0, run = 0;
@@ -276,7 +321,7 @@ __device__ double sample_iv(double kappa, double theta, double sigma, double dof
             return 0.0;
         }
         const int j = n + 1;
-        const cplx p = phi_eval(kappa, sigma2, nu, v_u, v_t, dt, j * h, err);
+        const cplx p = phi_node(P, j * h, err);
         if (*err != kErrNone) return 0.0;
         if (n < nc.cap) nc.base[(size_t)n * nc.stride] = p.re;
         const double mag = (2.0 / kPi) * cabs_(p) / j;
@@ -292,11 +337,22 @@ __device__ double sample_iv(double kappa, double theta, double sigma, double dof
     if (x > 0.9 * hi) x = 0.9 * hi;
     for (int it = 0; it < kNewtonMaxIter; ++it) {
         double f = h * x / kPi, d1 = h / kPi, d2 = 0.0;
+        // sin / cos (j h x) by rotation from (h x), re-seeded from sincos
+        // every kRotSeed nodes (drift ~ 1e-16 per node): the reference's
+        // per-node sin / cos to ~1e-15
+        double sr, cr, sx = 0.0, cxv = 1.0;
+        sincos(h * x, &sr, &cr);
         for (int j = 1; j <= n; ++j) {
             const double s_j = j * h;
             const double rp = nc.re(j - 1, err);
-            const double sx = sin(s_j * x), cxv = cos(s_j * x);
-            f += (2.0 / kPi) * sx / j * rp;
+            if ((j - 1) % kRotSeed == 0) {
+                sincos(s_j * x, &sx, &cxv);
+            } else {
+                const double sn = sx * cr + cxv * sr;
+                cxv = cxv * cr - sx * sr;
+                sx = sn;
+            }
+            f += (2.0 / kPi) * sx * inv_int(j) * rp;
             d1 += (2.0 * h / kPi) * cxv * rp;
             d2 -= (2.0 * h / kPi) * s_j * sx * rp;
         }
