@@ -232,18 +232,6 @@ struct NodeCache {
     }
 };
 
-// 1 / j for the Fourier-series weights: a constant-memory table (the loop
-// index is warp-uniform, so the load broadcasts) instead of a division
-constexpr int kInvTable = 512;
-struct InvIntTable {
-    double v[kInvTable];
-    constexpr InvIntTable() : v() {
-        for (int j = 1; j < kInvTable; ++j) v[j] = 1.0 / j;  // IEEE division, as on the device
-    }
-};
-__constant__ InvIntTable c_inv_int = InvIntTable();
-__device__ __forceinline__ double inv_int(int j) { return j < kInvTable ? c_inv_int.v[j] : 1.0 / j; }
-
 __device__ double cdf_at(double x, double h, int n, const NodeCache& nc, int* err) {
     double f = h * x / kPi;
     for (int j = 1; j <= n; ++j) f += (2.0 / kPi) * sin(j * h * x) / j * nc.re(j - 1, err);
@@ -342,17 +330,22 @@ __device__ double sample_iv(double kappa, double theta, double sigma, double dof
         // per-node sin / cos to ~1e-15
         double sr, cr, sx = 0.0, cxv = 1.0;
         sincos(h * x, &sr, &cr);
+        double rp_next = nc.re(0, err);  // node loads issue one node ahead
+        int seed = 0;
         for (int j = 1; j <= n; ++j) {
             const double s_j = j * h;
-            const double rp = nc.re(j - 1, err);
-            if ((j - 1) % kRotSeed == 0) {
+            const double rp = rp_next;
+            if (j < n) rp_next = nc.re(j, err);
+            if (seed == 0) {
                 sincos(s_j * x, &sx, &cxv);
+                seed = kRotSeed;
             } else {
                 const double sn = sx * cr + cxv * sr;
                 cxv = cxv * cr - sx * sr;
                 sx = sn;
             }
-            f += (2.0 / kPi) * sx * inv_int(j) * rp;
+            --seed;
+            f += (2.0 / kPi) * sx * __drcp_rn((double)j) * rp;
             d1 += (2.0 * h / kPi) * cxv * rp;
             d2 -= (2.0 * h / kPi) * s_j * sx * rp;
         }
