@@ -120,7 +120,7 @@ HMC_EXACT_FN cplx bessel_series(double nu, cplx z, int* err) {
 // (same operations on the same inputs) and removes one of the two series.
 struct PhiPath {
     double kappa, sigma2, nu, tau;
-    double ek, one_m_ek, kb, vs, w, log1m_ek;
+    double ek, one_m_ek, kb, vs, w, log1m_ek, ekh_inv;  // ekh_inv = e^{kappa tau / 2}
     cplx den;      // bessel_series(nu, w coeff_k)
     int den_err;   // its error code (kErrNone = 0)
 };
@@ -136,6 +136,7 @@ HMC_EXACT_FN PhiPath phi_path(double kappa, double sigma2, double nu, double v_u
     P.kb = kappa * (1.0 + P.ek) / (1.0 - P.ek);
     P.vs = (v_u + v_t) / sigma2;
     const double ekh = exp(-0.5 * kappa * tau);
+    P.ekh_inv = exp(0.5 * kappa * tau);
     const double coeff_k = 4.0 * kappa * ekh / (sigma2 * (1.0 - ekh * ekh));
     P.w = sqrt(v_u * v_t);
     P.log1m_ek = log(1.0 - P.ek);
@@ -148,13 +149,15 @@ HMC_EXACT_FN cplx phi_node(const PhiPath& P, double a, int* err) {
     if (a == 0.0) return cx(1.0);
     const double kappa = P.kappa, sigma2 = P.sigma2, nu = P.nu, tau = P.tau;
     const cplx g = csqrt_(cx(kappa * kappa, -2.0 * sigma2 * a));
-    const cplx eg = cexp_(cx(-g.re * tau, -g.im * tau));
+    // e^{-g tau / 2} once: e^{-g tau} is its square and the lead factor's
+    // e^{-(g - kappa) tau / 2} is it times e^{kappa tau / 2} (two complex
+    // exponentials fewer per node than the reference's formula)
+    const cplx egh = cexp_(-0.5 * (g * cx(tau)));
+    const cplx eg = egh * egh;
     const cplx one = cx(1.0);
-    const cplx lead = (g * cexp_(-0.5 * ((g - cx(kappa)) * cx(tau))) * cx(P.one_m_ek)) /
-                      (cx(kappa) * (one - eg));
+    const cplx lead = (g * (P.ekh_inv * egh) * cx(P.one_m_ek)) / (cx(kappa) * (one - eg));
     const cplx bracket = cx(P.kb) - (g * (one + eg)) / (one - eg);
     const cplx expo = cexp_(P.vs * bracket);
-    const cplx egh = cexp_(-0.5 * (g * cx(tau)));
     const cplx coeff_g = (4.0 * (g * egh)) / (cx(sigma2) * (one - egh * egh));
     const cplx log_q = clog_(g / kappa) - 0.5 * ((g - cx(kappa)) * cx(tau)) + cx(P.log1m_ek) -
                        clog_(one - eg);
