@@ -235,6 +235,35 @@ struct NodeCache {
     }
 };
 
+// F(x) - the CDF of the Fourier-series inversion -- and its first two
+// derivatives accumulated node by node (the reference's Newton sums,
+// _core.pyx:276-287); sin / cos (j h x) by rotation from (h x), re-seeded
+// from sincos every kRotSeed nodes (drift ~1e-16 per node: the reference's
+// per-node sin / cos to ~1e-15)
+struct NewtonSums {
+    double h, x, f, d1, d2, sr, cr, sx, cxv;
+    int seed;
+    __device__ NewtonSums(double h_, double x_) : h(h_), x(x_), f(h_ * x_ / kPi), d1(h_ / kPi), d2(0.0),
+                                                  sx(0.0), cxv(1.0), seed(0) {
+        sincos(h * x, &sr, &cr);
+    }
+    __device__ __forceinline__ void add(int j, double rp) {
+        const double s_j = j * h;
+        if (seed == 0) {
+            sincos(s_j * x, &sx, &cxv);
+            seed = kRotSeed;
+        } else {
+            const double sn = sx * cr + cxv * sr;
+            cxv = cxv * cr - sx * sr;
+            sx = sn;
+        }
+        --seed;
+        f += (2.0 / kPi) * sx * __drcp_rn((double)j) * rp;
+        d1 += (2.0 * h / kPi) * cxv * rp;
+        d2 -= (2.0 * h / kPi) * s_j * sx * rp;
+    }
+};
+
 __device__ double cdf_at(double x, double h, int n, const NodeCache& nc, int* err) {
     double f = h * x / kPi;
     for (int j = 1; j <= n; ++j) f += (2.0 / kPi) * sin(j * h * x) / j * nc.re(j - 1, err);
@@ -305,6 +334,14 @@ __device__ double sample_iv(double kappa, double theta, double sigma, double dof
     nc.P = &P;
     nc.h = h;
 
+    // the first Newton iterate is known before the nodes: its sums are
+    // accumulated while the nodes are generated (same order, same
+    // arithmetic as a separate pass), saving one pass over the nodes
+    double lo = 0.0, hi = 2.0 * kPi / h, x = mean;
+    if (x < 1e-3 * hi) x = 1e-3 * hi;
+    if (x > 0.9 * hi) x = 0.9 * hi;
+    NewtonSums first(h, x);
+
     int n = 0, run = 0;
     while (run < kTailRun) {
         if (n >= kMaxNodes) {
@@ -315,6 +352,7 @@ __device__ double sample_iv(double kappa, double theta, double sigma, double dof
         const cplx p = phi_node(P, j * h, err);
         if (*err != kErrNone) return 0.0;
         if (n < nc.cap) nc.base[(size_t)n * nc.stride] = p.re;
+        first.add(j, p.re);
         const double mag = (2.0 / kPi) * cabs_(p) / j;
         if (mag < kTailTol)
             ++run;
@@ -323,35 +361,18 @@ __device__ double sample_iv(double kappa, double theta, double sigma, double dof
         ++n;
     }
 
-    double lo = 0.0, hi = 2.0 * kPi / h, x = mean;
-    if (x < 1e-3 * hi) x = 1e-3 * hi;
-    if (x > 0.9 * hi) x = 0.9 * hi;
     for (int it = 0; it < kNewtonMaxIter; ++it) {
-        double f = h * x / kPi, d1 = h / kPi, d2 = 0.0;
-        // sin / cos (j h x) by rotation from (h x), re-seeded from sincos
-        // every kRotSeed nodes (drift ~ 1e-16 per node): the reference's
-        // per-node sin / cos to ~1e-15
-        double sr, cr, sx = 0.0, cxv = 1.0;
-        sincos(h * x, &sr, &cr);
-        double rp_next = nc.re(0, err);  // node loads issue one node ahead
-        int seed = 0;
-        for (int j = 1; j <= n; ++j) {
-            const double s_j = j * h;
-            const double rp = rp_next;
-            if (j < n) rp_next = nc.re(j, err);
-            if (seed == 0) {
-                sincos(s_j * x, &sx, &cxv);
-                seed = kRotSeed;
-            } else {
-                const double sn = sx * cr + cxv * sr;
-                cxv = cxv * cr - sx * sr;
-                sx = sn;
+        NewtonSums ns = first;
+        if (it > 0) {
+            ns = NewtonSums(h, x);
+            double rp_next = nc.re(0, err);  // node loads issue one node ahead
+            for (int j = 1; j <= n; ++j) {
+                const double rp = rp_next;
+                if (j < n) rp_next = nc.re(j, err);
+                ns.add(j, rp);
             }
-            --seed;
-            f += (2.0 / kPi) * sx * __drcp_rn((double)j) * rp;
-            d1 += (2.0 * h / kPi) * cxv * rp;
-            d2 -= (2.0 * h / kPi) * s_j * sx * rp;
         }
+        const double f = ns.f, d1 = ns.d1, d2 = ns.d2;
         const double efun = f - u;
         if (fabs(efun) < kNewtonTol) return x;
         if (efun > 0.0) {
