@@ -64,12 +64,13 @@ __device__ __forceinline__ cplx operator/(cplx a, double s) {
 }
 // Smith's algorithm (robust complex division)
 __device__ __forceinline__ cplx operator/(cplx a, cplx b) {
+    // (one reciprocal of d instead of two divisions by it)
     if (fabs(b.re) >= fabs(b.im)) {
-        const double r = b.im / b.re, d = b.re + b.im * r;
-        return {(a.re + a.im * r) / d, (a.im - a.re * r) / d};
+        const double r = b.im / b.re, id = 1.0 / (b.re + b.im * r);
+        return {(a.re + a.im * r) * id, (a.im - a.re * r) * id};
     }
-    const double r = b.re / b.im, d = b.re * r + b.im;
-    return {(a.re * r + a.im) / d, (a.im * r - a.re) / d};
+    const double r = b.re / b.im, id = 1.0 / (b.re * r + b.im);
+    return {(a.re * r + a.im) * id, (a.im * r - a.re) * id};
 }
 // |a|: the magnitudes here are moderate (Bessel arguments <= 50, series
 // values <= e^50), so sqrt(re^2 + im^2) cannot over/underflow where hypot's
