@@ -160,8 +160,13 @@ HMC_EXACT_FN cplx phi_node(const PhiPath& P, double a, int* err) {
     const cplx bracket = cx(P.kb) - (g * (one + eg)) / (one - eg);
     const cplx expo = cexp_(P.vs * bracket);
     const cplx coeff_g = (4.0 * (g * egh)) / (cx(sigma2) * (one - egh * egh));
-    const cplx log_q = clog_(g / kappa) - 0.5 * ((g - cx(kappa)) * cx(tau)) + cx(P.log1m_ek) -
-                       clog_(one - eg);
+    // log q = log(g / kappa) - (g - kappa) tau / 2 + log(1 - e^{-kappa tau}) - log(1 - e^{-g tau}),
+    // the two real logarithms merged into one (the arguments keep their own
+    // atan2 branches, exactly as the two complex logarithms)
+    const cplx gk = g / kappa, ome = one - eg;
+    const cplx half_gt = 0.5 * ((g - cx(kappa)) * cx(tau));
+    const cplx log_q = {0.5 * log(norm2_(gk) / norm2_(ome)) - half_gt.re + P.log1m_ek,
+                        atan2(gk.im, gk.re) - half_gt.im - atan2(ome.im, ome.re)};
     const cplx num = cexp_(nu * log_q) * bessel_series(nu, P.w * coeff_g, err);
     if (P.den_err != kErrNone) *err = P.den_err;
     return lead * expo * (num / P.den);
