@@ -14,7 +14,7 @@
 // few bucketed moments (hmc_api.cu surface_finalize).  Cost per path and
 // maturity is O(log K) instead of O(K).
 //
-// Histograms are integer fixed point (linear moments 2^-10, quadratic 2^2,
+// Histograms are integer fixed point (linear moments to 2^-10, quadratic to 2^-2,
 // counts exact; int32 per block, int64 per run): integer addition is
 // associative, so block order, grid size and GPU count cannot change a
 // single bit of the result -- multi-GPU runs all-reduce the integer

@@ -101,3 +101,27 @@ def test_validation():
         surface(p, STRIKES, [0.3, 1.0], _cfg(64))
     with pytest.raises(UnsupportedProduct):
         surface(p, STRIKES, MATS, _cfg(64, precision="fp64"))
+
+
+@pytest.mark.parametrize("qmc", [{}, dict(sampler="sobol", sobol_highdim_ack=True, sobol_scramble=True)])
+def test_checkpoints_at_every_tri_pack_offset(qmc):
+    """Maturities on steps 1, 5, 9 and 13 of a 13-step grid put the
+    checkpoints at every offset inside the kernel's three-step Philox blocks
+    (and across Sobol table refills); a uniform strike grid takes the
+    arithmetic bucket path.  Every point equals the single-product engine."""
+    p = HestonParams(**BENCH_PARAMS)
+    steps = (1, 5, 9, 13)
+    mats = [k / 13.0 for k in steps]
+    strikes = [90.0, 95.0, 100.0, 105.0, 110.0]
+    cfg = lambda n: SimConfig(scheme="milstein", n_paths=20_000, n_steps=n, n_runs=1, seed=7, **qmc)  # noqa: E731
+    res = surface(p, strikes, mats, cfg(13))
+    for mi, (T, n) in enumerate(zip(mats, steps)):
+        for j, K in enumerate(strikes):
+            for style in ("european", "asian_arithmetic"):
+                dates = daily_fixings(T, n) if style != "european" else ()
+                g = greeks(p, OptionSpec(style, "call", K, T, 100.0, averaging_times=dates), cfg(n))
+                for q in ("price", "delta", "rho", "gamma", "vega"):
+                    tol = 1e-3 if q == "vega" else 3e-5
+                    scale = max(abs(g[q].estimate), 1e-3)
+                    assert abs(res.estimate[style][q][mi, j] - g[q].estimate) <= tol * scale + 1e-6, \
+                        (style, T, K, q, res.estimate[style][q][mi, j], g[q].estimate)
