@@ -150,26 +150,33 @@ HMC_EXACT_FN cplx phi_node(const PhiPath& P, double a, int* err) {
     if (a == 0.0) return cx(1.0);
     const double kappa = P.kappa, sigma2 = P.sigma2, nu = P.nu, tau = P.tau;
     const cplx g = csqrt_(cx(kappa * kappa, -2.0 * sigma2 * a));
-    // e^{-g tau / 2} once: e^{-g tau} is its square and the lead factor's
-    // e^{-(g - kappa) tau / 2} is it times e^{kappa tau / 2} (two complex
-    // exponentials fewer per node than the reference's formula)
+    // The reference's formula, regrouped (same mathematics, last-ulp
+    // differences): e^{-g tau / 2} once -- e^{-g tau} is its square and the
+    // lead factor's e^{-(g - kappa) tau / 2} is it times e^{kappa tau / 2};
+    // the three quotients by 1 - e^{-g tau} share one reciprocal (the
+    // Bessel argument's 1 - e^{-g tau}... is the same 1 - egh^2), and
+    // g e^{-g tau / 2} / (1 - e^{-g tau}) is shared by the lead factor and
+    // the Bessel argument; the two outer exponentials are one.
     const cplx egh = cexp_(-0.5 * (g * cx(tau)));
     const cplx eg = egh * egh;
     const cplx one = cx(1.0);
-    const cplx lead = (g * (P.ekh_inv * egh) * cx(P.one_m_ek)) / (cx(kappa) * (one - eg));
-    const cplx bracket = cx(P.kb) - (g * (one + eg)) / (one - eg);
-    const cplx expo = cexp_(P.vs * bracket);
-    const cplx coeff_g = (4.0 * (g * egh)) / (cx(sigma2) * (one - egh * egh));
+    const cplx ome = one - eg;
+    const cplx inv_ome = one / ome;
+    const cplx ge = (g * egh) * inv_ome;
+    const cplx lead = (P.ekh_inv * P.one_m_ek / kappa) * ge;
+    const cplx bracket = cx(P.kb) - (g * (one + eg)) * inv_ome;
+    const cplx coeff_g = (4.0 / sigma2) * ge;
     // log q = log(g / kappa) - (g - kappa) tau / 2 + log(1 - e^{-kappa tau}) - log(1 - e^{-g tau}),
     // the two real logarithms merged into one (the arguments keep their own
     // atan2 branches, exactly as the two complex logarithms)
-    const cplx gk = g / kappa, ome = one - eg;
+    const cplx gk = g / kappa;
     const cplx half_gt = 0.5 * ((g - cx(kappa)) * cx(tau));
     const cplx log_q = {0.5 * log(norm2_(gk) / norm2_(ome)) - half_gt.re + P.log1m_ek,
                         atan2(gk.im, gk.re) - half_gt.im - atan2(ome.im, ome.re)};
-    const cplx num = cexp_(nu * log_q) * bessel_series(nu, P.w * coeff_g, err);
+    const cplx expo = cexp_(P.vs * bracket + nu * log_q);   // e^{vs bracket} q^nu
+    const cplx ser = bessel_series(nu, P.w * coeff_g, err);
     if (P.den_err != kErrNone) *err = P.den_err;
-    return lead * expo * (num / P.den);
+    return lead * expo * (ser / P.den.re);   // the denominator series has a real argument: real
 }
 
 HMC_EXACT_FN double ndtri_d(double u) {
