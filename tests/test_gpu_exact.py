@@ -157,3 +157,63 @@ def test_exact_chunks_split_bit_identical(params):
     whole = chunks(0, cfg.n_paths)
     parts = np.concatenate([chunks(0, 16384), chunks(16384, 3 * 16384), chunks(3 * 16384, cfg.n_paths)], axis=1)
     np.testing.assert_array_equal(whole, parts)
+
+
+# ---------------------------------------------------------------------------
+# The reference's own exact-scheme properties (tests/test_exact.py:75-96,
+# tests/test_ivlaw.py:122-137), run through the GPU backend plugin.
+# ---------------------------------------------------------------------------
+def _key(seed):
+    from oracle import derive_key, root_key
+    return int(derive_key(root_key(seed), 0))
+
+
+def test_exact_martingale(params):
+    """Discounted terminal mean over 10^5 exact paths equals S0 within 3 SE."""
+    import math
+    obs = cuda_backend.exact_batch(params, 100.0, np.array([0.0, 1.0]), np.array([1], dtype=np.int64),
+                                   0, 100_000, _key(11), None)
+    disc = math.exp(-params.r) * obs[:, 0]
+    assert abs(disc.mean() - 100.0) < 3.0 * disc.std(ddof=1) / math.sqrt(disc.size)
+
+
+def test_exact_composability_across_partitions(params):
+    """One step over [0, 1] and two steps over [0, .5], [.5, 1] give the same
+    law of S_T (two-sample KS)."""
+    from scipy import stats
+    one = cuda_backend.exact_batch(params, 100.0, np.array([0.0, 1.0]), np.array([1], dtype=np.int64),
+                                   0, 50_000, _key(21), None)[:, 0]
+    two = cuda_backend.exact_batch(params, 100.0, np.array([0.0, 0.5, 1.0]), np.array([0, 1], dtype=np.int64),
+                                   0, 50_000, _key(22), None)[:, 0]
+    assert stats.ks_2samp(one, two).pvalue > 0.01
+
+
+def test_exact_tiny_dt_exceeds_series_validity(params):
+    """The Bessel argument grows like 1/dt: a 1e-4 step is reported, not
+    returned as garbage (the reference raises BesselNonConvergence)."""
+    with pytest.raises(BesselNonConvergence):
+        cuda_backend.exact_batch(params, 100.0, np.array([0.0, 1e-4]), np.array([1], dtype=np.int64),
+                                 0, 64, _key(5), None)
+
+
+def test_exact_vanishing_vol_of_vol_collapses_to_mean_path():
+    """sigma -> 0: the integrated variance is the deterministic mean path, so
+    S_T is lognormal with that variance (the reference's degenerate branch)."""
+    import math
+    from paper_2309_10477_b200 import DEFAULT_PARAMS
+    p = HestonParams(**dict(DEFAULT_PARAMS, sigma=1e-7))
+    obs = cuda_backend.exact_batch(p, 100.0, np.array([0.0, 1.0]), np.array([1], dtype=np.int64),
+                                   0, 50_000, _key(3), None)
+    iv = p.theta + (p.v0 - p.theta) * (1.0 - math.exp(-p.kappa)) / p.kappa
+    logs = np.log(obs[:, 0] / 100.0)
+    assert abs(logs.var(ddof=1) - iv) < 0.03 * iv
+    assert abs(logs.mean() - (p.r - 0.5 * iv)) < 3.0 * math.sqrt(iv / logs.size)
+
+
+def test_exact_zero_start_variance():
+    """v0 = 0 is a valid start (reference test_exact.py:45-47)."""
+    from paper_2309_10477_b200 import DEFAULT_PARAMS
+    p = HestonParams(**dict(DEFAULT_PARAMS, v0=0.0))
+    obs = cuda_backend.exact_batch(p, 100.0, np.array([0.0, 0.5]), np.array([1], dtype=np.int64),
+                                   0, 4096, _key(9), None)
+    assert np.all(np.isfinite(obs)) and np.all(obs[:, 0] > 0.0)
