@@ -71,3 +71,27 @@ def test_run_experiment_paths_sweep_shrinks_spread(params, euro_call):
 def test_run_experiment_greeks_rows(params, euro_call):
     rows = run_experiment([cfg(n_paths=4096)], params, euro_call, want_greeks=True)
     assert {"price", "delta", "rho", "gamma", "vega"} <= set(rows[0]["summaries"])
+
+
+def test_schemes_agree_as_vol_of_vol_vanishes(euro_call):
+    """reference tests/test_schemes.py:80-88: the Milstein correction is
+    O(sigma^2), so on the same normals Euler and Milstein coincide as
+    sigma -> 0 (fp32 path state: to ~1e-6 relative)."""
+    from paper_2309_10477_b200 import DEFAULT_PARAMS, HestonParams
+    p = HestonParams(**dict(DEFAULT_PARAMS, sigma=1e-6))
+    e = price(p, euro_call, cfg(scheme="euler", n_paths=20_000, n_steps=64))
+    m = price(p, euro_call, cfg(scheme="milstein", n_paths=20_000, n_steps=64))
+    np.testing.assert_allclose(e.per_run_values, m.per_run_values, rtol=1e-5)
+
+
+def test_variance_truncation_under_stress(euro_call):
+    """reference tests/test_schemes.py:70-78: far outside the Feller
+    condition the truncated variance keeps every path finite (fp32 kernel,
+    Euler and Milstein, full Greeks)."""
+    from paper_2309_10477_b200 import HestonParams
+    p = HestonParams(kappa=0.5, theta=0.09, sigma=2.0, rho=-0.9, r=0.02, v0=0.09)
+    for scheme in ("euler", "milstein"):
+        g = greeks(p, euro_call, cfg(scheme=scheme, n_paths=20_000, n_steps=64))
+        for q, s in g.items():
+            assert np.all(np.isfinite(s.per_run_values)), (scheme, q)
+        assert g["price"].estimate > 0.0
