@@ -210,3 +210,16 @@ def run_experiment(grid: list[SimConfig], params: HestonParams, spec: OptionSpec
                      "paths": config.n_paths, "steps": config.n_steps,
                      "runs": config.n_runs, "summaries": res})
     return rows
+
+
+def warm_up() -> None:
+    """Create the CUDA context, load ``libhmc.so`` and launch one tiny job,
+    so a fresh process (the CLI) does not book that one-time start-up as the
+    ``wall_ms`` of its first timed run.  No-op without a CUDA device (the
+    real call then raises :class:`DeviceError`)."""
+    import torch
+    if not torch.cuda.is_available():
+        return
+    from .model import BENCH_PARAMS
+    price(HestonParams(**BENCH_PARAMS), OptionSpec("european", "call", 100.0, 1.0, 100.0),
+          SimConfig(scheme="milstein", n_paths=128, n_steps=3, n_runs=1))
