@@ -248,6 +248,18 @@ struct NodeCache {
     }
 };
 
+// 1 / j for the Fourier-series weights: a constant-memory table (the node
+// index is warp-uniform, so the load broadcasts) instead of a division
+constexpr int kInvTable = 512;
+struct InvIntTable {
+    double v[kInvTable];
+    constexpr InvIntTable() : v() {
+        for (int j = 1; j < kInvTable; ++j) v[j] = 1.0 / j;  // IEEE quotient, as __drcp_rn
+    }
+};
+__constant__ InvIntTable c_inv_int = InvIntTable();
+__device__ __forceinline__ double inv_int(int j) { return j < kInvTable ? c_inv_int.v[j] : __drcp_rn((double)j); }
+
 // F(x) - the CDF of the Fourier-series inversion -- and its first two
 // derivatives accumulated node by node (the reference's Newton sums,
 // _core.pyx:276-287); sin / cos (j h x) by rotation from (h x), re-seeded
@@ -271,7 +283,7 @@ struct NewtonSums {
             sx = sn;
         }
         --seed;
-        f += (2.0 / kPi) * sx * __drcp_rn((double)j) * rp;
+        f += (2.0 / kPi) * sx * inv_int(j) * rp;
         d1 += (2.0 * h / kPi) * cxv * rp;
         d2 -= (2.0 * h / kPi) * s_j * sx * rp;
     }
@@ -366,8 +378,9 @@ __device__ double sample_iv(double kappa, double theta, double sigma, double dof
         if (*err != kErrNone) return 0.0;
         if (n < nc.cap) nc.base[(size_t)n * nc.stride] = p.re;
         first.add(j, p.re);
-        const double mag = (2.0 / kPi) * cabs_(p) / j;
-        if (mag < kTailTol)
+        // (2/pi) |p| / j < tol, compared squared
+        const double tj = kTailTol * j;
+        if ((4.0 / (kPi * kPi)) * norm2_(p) < tj * tj)
             ++run;
         else
             run = 0;
