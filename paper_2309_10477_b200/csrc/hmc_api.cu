@@ -378,7 +378,7 @@ __global__ void box_muller_kat_kernel(const uint4* __restrict__ w, int n, Kernel
         tri_unpack(x, fr, fa);
         for (int k = 0; k < 3; ++k) {
             float z1, z2;
-            box_muller_f(fr[k], fa[k], x.x << (31 - k), a, z1, z2);
+            box_muller_f(fr[k], fa[k], a, z1, z2);
             out[6 * i + 2 * k] = z1;
             out[6 * i + 2 * k + 1] = z2;
         }

@@ -83,7 +83,6 @@ __device__ __forceinline__ cplx cexp_(cplx a) {
     sincos(a.im, &s, &c);
     return {e * c, e * s};
 }
-__device__ __forceinline__ cplx clog_(cplx a) { return {log(cabs_(a)), atan2(a.im, a.re)}; }
 // principal square root
 __device__ __forceinline__ cplx csqrt_(cplx a) {
     if (a.re == 0.0 && a.im == 0.0) return {0.0, a.im};

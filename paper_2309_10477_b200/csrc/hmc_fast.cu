@@ -17,12 +17,9 @@
 //                L' = L + sqrt(v) (sqrt(dt) z1 log2 e) - v dt/2 log2 e
 //              S_k = E_k 2^{L_k}, E_k = S0 e^{r t_k}, only at fixing dates
 //
-// The loop is bound jointly by instruction issue and the MUFU (XU) pipe
-// (DESIGN.md "roofline").  Build-time switches trade MUFU ops for FMA-pipe
-// polynomials:
-//   HMC_SINCOS_POLY  Box-Muller angle via sin/cos polynomials (-2 MUFU/step)
-//   HMC_EX2_POLY     number of trajectories (0..3) whose 2^L uses a
-//                    polynomial instead of MUFU.EX2 (-1 MUFU/step each)
+// The loop is bound by the MUFU (XU) pipe at ~86 %;
+// the FMA-pipe substitutions tried against it (sin/cos and ex2 polynomials,
+// scalar and paired FFMA2) are recorded with their timings in DESIGN.md.
 #include <cuda_runtime.h>
 
 #include "hmc_device.cuh"
@@ -183,7 +180,7 @@ __global__ void HMC_BOUNDS fast_greeks_kernel(const KernelArgs a,
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
                 float z1l, sz2;
-                box_muller_f(fr[i], fa[i], x.x << (31 - i), a, z1l, sz2);
+                box_muller_f(fr[i], fa[i], a, z1l, sz2);
                 step<FIX, GREEKS, FIX == kFixLast>(st, k + i, z1l, sz2, a);
             }
             k += 3;
@@ -194,7 +191,7 @@ __global__ void HMC_BOUNDS fast_greeks_kernel(const KernelArgs a,
             tri_unpack(x, fr, fa);
             for (int i = 0; k + i <= a.n_sim; ++i) {
                 float z1l, sz2;
-                box_muller_f(fr[i], fa[i], x.x << (31 - i), a, z1l, sz2);
+                box_muller_f(fr[i], fa[i], a, z1l, sz2);
                 step<FIX, GREEKS, FIX == kFixLast>(st, k + i, z1l, sz2, a);
             }
         }

@@ -10,25 +10,6 @@
 
 #include "hmc_device.cuh"
 
-#ifndef HMC_SINCOS_POLY
-#define HMC_SINCOS_POLY 0
-#endif
-#ifndef HMC_EX2_POLY
-#define HMC_EX2_POLY 0
-#endif
-#ifndef HMC_SOBOL_VOTE
-#define HMC_SOBOL_VOTE 1     // Sobol quantile: warp-voted tail branches (all 32 lanes must be active;
-                             // 0 = the divergent if/else without the extreme-cell branch, experiments only)
-#endif
-#ifndef HMC_SQRT_RSQ
-#define HMC_SQRT_RSQ 0
-#endif
-#ifndef HMC_EX2_DELTA
-#define HMC_EX2_DELTA 0      // bumped trajectories' 2^L from the base one (guarded)
-#endif
-#ifndef HMC_EX2_PAIR_POLY
-#define HMC_EX2_PAIR_POLY 0  // bumped pair's 2^L by a paired FMA polynomial instead of 2 MUFU.EX2
-#endif
 
 namespace hmc {
 
@@ -47,61 +28,8 @@ __device__ __forceinline__ float sqrta(float x) {
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
-__device__ __forceinline__ float rsqrta(float x) {
-    float y;
-    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-// sqrt(v) of a variance (v >= 0): MUFU.SQRT, or v * MUFU.RSQ(v) (exact 0 at v = 0)
-__device__ __forceinline__ float sqrt_var(float v) {
-#if HMC_SQRT_RSQ
-    return v * rsqrta(fmaxf(v, 1e-30f));
-#else
-    return sqrta(v);
-#endif
-}
-
+// a float2 with both halves x (scalar operand of the paired FFMA2/FMUL2)
 __device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
-
-// 2^x on the FMA pipe: x = j + f, |f| <= 1/2, 2^f by a degree-6 Taylor
-// polynomial (rel. err 1.6e-7), exponent added with one LEA.
-__device__ __forceinline__ float ex2_poly(float x) {
-    const float magic = 12582912.0f;  // 1.5 * 2^23: rounds to integer
-    x = fmaxf(x, -125.0f);            // keep the exponent add in range
-    const float m = x + magic;
-    const float f = x - (m - magic);
-    float p = 1.5403530393381606e-4f;
-    p = fmaf(p, f, 1.3333558146428441e-3f);
-    p = fmaf(p, f, 9.6181291076284772e-3f);
-    p = fmaf(p, f, 5.5504108664821576e-2f);
-    p = fmaf(p, f, 2.4022650695910071e-1f);
-    p = fmaf(p, f, 6.9314718055994531e-1f);
-    p = fmaf(p, f, 1.0f);
-    return __uint_as_float(__float_as_uint(p) + (__float_as_uint(m) << 23));
-}
-
-template <int POLY>
-__device__ __forceinline__ float ex2_sel(float x) {
-    if (POLY) return ex2_poly(x);
-    return ex2a(x);
-}
-
-// ex2_poly on a pair with paired FFMA2/FADD2 (the same per-lane arithmetic)
-__device__ __forceinline__ float2 ex2_poly2(float2 x) {
-    const float magic = 12582912.0f;
-    x = make_float2(fmaxf(x.x, -125.0f), fmaxf(x.y, -125.0f));
-    const float2 m = __fadd2_rn(x, make_float2(magic, magic));
-    const float2 f = __ffma2_rn(__fadd2_rn(m, make_float2(-magic, -magic)), make_float2(-1.0f, -1.0f), x);
-    float2 p = make_float2(1.5403530393381606e-4f, 1.5403530393381606e-4f);
-    p = __ffma2_rn(p, f, make_float2(1.3333558146428441e-3f, 1.3333558146428441e-3f));
-    p = __ffma2_rn(p, f, make_float2(9.6181291076284772e-3f, 9.6181291076284772e-3f));
-    p = __ffma2_rn(p, f, make_float2(5.5504108664821576e-2f, 5.5504108664821576e-2f));
-    p = __ffma2_rn(p, f, make_float2(2.4022650695910071e-1f, 2.4022650695910071e-1f));
-    p = __ffma2_rn(p, f, make_float2(6.9314718055994531e-1f, 6.9314718055994531e-1f));
-    p = __ffma2_rn(p, f, make_float2(1.0f, 1.0f));
-    return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(m.x) << 23)),
-                       __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(m.y) << 23)));
-}
 
 // uniform in [1, 2) from the top 23 bits of x: one LEA.HI
 __device__ __forceinline__ float one_to_two(uint32_t x) {
@@ -110,42 +38,18 @@ __device__ __forceinline__ float one_to_two(uint32_t x) {
 
 // Box-Muller on two Philox words; returns the step shocks
 //   z1l = sqrt(dt) z1 log2(e),   sz2 = sigma sqrt(dt) (rho z1 + sqrt(1-rho^2) zb)
-__device__ __forceinline__ void sincos_turns(float fa, uint32_t sgn, float& sn, float& cs) {
-#if HMC_SINCOS_POLY
-    // angle in [-pi/2, pi/2) from fa in [1, 2), sin/cos by Taylor polynomials
-    // (abs err 6e-8); a random sign bit (bit 31 of sgn) flips cos to cover
-    // the left half circle
-    const float r = fmaf(fa, 2.0f, -3.0f);                   // [-1, 1)
-    const float r2 = r * r;
-    float ps = -3.598843235212084e-06f;
-    ps = fmaf(ps, r2, 1.6044118478735975e-04f);
-    ps = fmaf(ps, r2, -4.681754135318687e-03f);
-    ps = fmaf(ps, r2, 7.969262624616703e-02f);
-    ps = fmaf(ps, r2, -6.459640975062462e-01f);
-    ps = fmaf(ps, r2, 1.5707963267948966f);
-    sn = ps * r;
-    float pc = 4.710874778818169e-07f;
-    pc = fmaf(pc, r2, -2.5202042373060596e-05f);
-    pc = fmaf(pc, r2, 9.192602748394263e-04f);
-    pc = fmaf(pc, r2, -2.0863480763352957e-02f);
-    pc = fmaf(pc, r2, 2.53669507901048e-01f);
-    pc = fmaf(pc, r2, -1.2337005501361697f);
-    pc = fmaf(pc, r2, 1.0f);
-    cs = __uint_as_float(__float_as_uint(pc) ^ (sgn & 0x80000000u));
-#else
+__device__ __forceinline__ void sincos_turns(float fa, float& sn, float& cs) {
     const float th = fmaf(fa, 6.28318530717958647692f, -9.42477796076937971538f);
     sn = __sinf(th);                                         // th in [-pi, pi)
     cs = __cosf(th);
-    (void)sgn;
-#endif
 }
 
-__device__ __forceinline__ void box_muller_f(float fr, float fa, uint32_t sgn, const KernelArgs& a,
+__device__ __forceinline__ void box_muller_f(float fr, float fa, const KernelArgs& a,
                                              float& z1l, float& sz2) {
     const float u1 = 2.0f - fr;                              // (0, 1]
     const float R = sqrta(lg2a(u1) * a.f_bm2);               // sqrt(dt) sqrt(-2 ln u1) log2 e
     float sn, cs;
-    sincos_turns(fa, sgn, sn, cs);
+    sincos_turns(fa, sn, cs);
     z1l = R * cs;
     sz2 = R * fmaf(a.f_cA, cs, a.f_cB * sn);
 }
@@ -178,7 +82,6 @@ __device__ __forceinline__ float sobol_normal_u(uint32_t x, float hx, float ht) 
     // w = -ln(4 tf (1 - tf)) = -ln2 (lg2(tf (1 - tf)) + 2)
     float w = fmaf(lg2a(tf * (1.0f - tf)), -0.69314718055994530942f, -1.38629436111989061883f);
     float p;
-#if HMC_SOBOL_VOTE
     // central branch for every lane; the tail branch (|2u - 1| > 0.9966,
     // 0.3 % of draws) only in warps where a lane needs it: a uniform vote
     // instead of a divergent if/else around both polynomials
@@ -220,31 +123,6 @@ __device__ __forceinline__ float sobol_normal_u(uint32_t x, float hx, float ht) 
             if (w >= 16.0f) return hi ? -z : z;
         }
     }
-#else
-    if (w < 5.0f) {
-        w = w - 2.5f;
-        p = 2.81022636e-08f;
-        p = fmaf(p, w, 3.43273939e-07f);
-        p = fmaf(p, w, -3.5233877e-06f);
-        p = fmaf(p, w, -4.39150654e-06f);
-        p = fmaf(p, w, 0.00021858087f);
-        p = fmaf(p, w, -0.00125372503f);
-        p = fmaf(p, w, -0.00417768164f);
-        p = fmaf(p, w, 0.246640727f);
-        p = fmaf(p, w, 1.50140941f);
-    } else {
-        w = sqrta(w) - 3.0f;
-        p = -0.000200214257f;
-        p = fmaf(p, w, 0.000100950558f);
-        p = fmaf(p, w, 0.00134934322f);
-        p = fmaf(p, w, -0.00367342844f);
-        p = fmaf(p, w, 0.00573950773f);
-        p = fmaf(p, w, -0.0076224613f);
-        p = fmaf(p, w, 0.00943887047f);
-        p = fmaf(p, w, 1.00167406f);
-        p = fmaf(p, w, 2.83297682f);
-    }
-#endif
     return p * xs;
 }
 
@@ -311,7 +189,7 @@ struct PathState32 {
 
 __device__ __forceinline__ void traj_step(float& v, float& L, float z1l, float sz2, float ck,
                                           const KernelArgs& a) {
-    const float s = sqrt_var(v);
+    const float s = sqrta(v);
     L = fmaf(s, z1l, L);
     L = fmaf(v, a.f_nhdt2, L);
     v = fmaxf(fmaf(s, sz2, fmaf(v, a.f_omkdt, ck)), 0.0f);
@@ -325,7 +203,7 @@ template <bool PAIR>
 __device__ __forceinline__ void traj_step2(float2& v, float2& L, float z1l, float sz2, float ck,
                                            const KernelArgs& a) {
     if (PAIR) {
-    const float2 s = make_float2(sqrt_var(v.x), sqrt_var(v.y));
+    const float2 s = make_float2(sqrta(v.x), sqrta(v.y));
     L = __ffma2_rn(s, f2(z1l), L);
     L = __ffma2_rn(v, f2(a.f_nhdt2), L);
     const float2 t = __ffma2_rn(s, f2(sz2), __ffma2_rn(v, f2(a.f_omkdt), f2(ck)));
@@ -345,46 +223,21 @@ __device__ __forceinline__ void advance(PathState32& st, float z1l, float sz2, c
 
 template <bool GREEKS, bool PAIR = false>
 __device__ __forceinline__ void fixing(PathState32& st, const float4 w) {
-    const float P = ex2_sel<(HMC_EX2_POLY >= 3)>(st.L0);
+    const float P = ex2a(st.L0);
     st.A0 = fmaf(P, w.x, st.A0);
     if (GREEKS) {
         st.T1 = fmaf(P, w.y, st.T1);
         st.Dp = fmaf(P, w.z, st.Dp);
         st.Dm = fmaf(P, w.w, st.Dm);
-#if HMC_EX2_DELTA
-        // the v0-bumped log-prices stay within |d| << 1 of the base one, so
-        // 2^{L+d} = 2^L (1 + d ln2 + (d ln2)^2/2 + (d ln2)^3/6) (rel. err
-        // < 6e-8 for |d| <= 0.05); a warp with any larger d uses MUFU.EX2
-        const float du = st.Lb.x - st.L0, dd = st.Lb.y - st.L0;
-        float Pu, Pd;
-        if (__all_sync(0xffffffffu, fmaxf(fabsf(du), fabsf(dd)) <= 0.05f)) {
-            auto e2 = [](float d) {
-                return fmaf(fmaf(fmaf(0.0555041086648216f, d, 0.2402265069591007f), d,
-                                 0.6931471805599453f), d, 1.0f);
-            };
-            Pu = P * e2(du);
-            Pd = P * e2(dd);
-        } else {
-            Pu = ex2a(st.Lb.x);
-            Pd = ex2a(st.Lb.y);
-        }
-        st.Ab = __ffma2_rn(make_float2(Pu, Pd), f2(w.x), st.Ab);
-#else
         // (carrying Au - A0 instead -- one more FADD per trajectory and
         // fixing -- shrinks Vega's fp32 error ~40x but costs 4 % of the
         // daily-fixing kernel: 10.66 -> 11.08 ms; not taken)
-#if HMC_EX2_PAIR_POLY
-        st.Ab = __ffma2_rn(ex2_poly2(st.Lb), f2(w.x), st.Ab);
-#else
         if (PAIR) {
-            st.Ab = __ffma2_rn(make_float2(ex2_sel<(HMC_EX2_POLY >= 1)>(st.Lb.x),
-                                           ex2_sel<(HMC_EX2_POLY >= 2)>(st.Lb.y)), f2(w.x), st.Ab);
+            st.Ab = __ffma2_rn(make_float2(ex2a(st.Lb.x), ex2a(st.Lb.y)), f2(w.x), st.Ab);
         } else {
-            st.Ab.x = fmaf(ex2_sel<(HMC_EX2_POLY >= 1)>(st.Lb.x), w.x, st.Ab.x);
-            st.Ab.y = fmaf(ex2_sel<(HMC_EX2_POLY >= 2)>(st.Lb.y), w.x, st.Ab.y);
+            st.Ab.x = fmaf(ex2a(st.Lb.x), w.x, st.Ab.x);
+            st.Ab.y = fmaf(ex2a(st.Lb.y), w.x, st.Ab.y);
         }
-#endif
-#endif
     }
 }
 

@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(kSurfThreads, kSurfMinBlocks) surface_kernel(c
 #pragma unroll
                 for (int i = 0; i < 3; ++i) {
                     float z1l, sz2;
-                    box_muller_f(fr[i], fa[i], x.x << (31 - i), a, z1l, sz2);
+                    box_muller_f(fr[i], fa[i], a, z1l, sz2);
                     step<kFixEvery, true>(st, k0 + i, z1l, sz2, a);
                 }
                 continue;
@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(kSurfThreads, kSurfMinBlocks) surface_kernel(c
                 const int k = k0 + i;
                 if (k > a.n_sim) break;
                 float z1l, sz2;
-                box_muller_f(fr[i], fa[i], x.x << (31 - i), a, z1l, sz2);
+                box_muller_f(fr[i], fa[i], a, z1l, sz2);
                 step<kFixEvery, true>(st, k, z1l, sz2, a);
                 if (k == next) {
                     surface_checkpoint(st, a, s, m, live, hist, sK, pow2, gacc);

@@ -20,7 +20,8 @@ VDIR = os.path.join(ROOT, "paper_2309_10477_b200", "_variants")
 
 VARIANTS = {
     "base": {},
-    "x_noweights": {"HMC_EXP_NO_WEIGHT_LOAD": 1},
+    "lb6": {"HMC_MIN_BLOCKS": 6},
+    "lb8": {"HMC_MIN_BLOCKS": 8},
 }
 
 
