@@ -62,3 +62,22 @@ def test_json_line_owns_stdout_under_torchrun():
     assert r.returncode == 0, r.stderr[-2000:]
     out = r.stdout.splitlines()
     assert len(out) == 1 and json.loads(out[0])["impl"] == "reference"
+
+
+def test_committed_b200_line_has_the_contract_keys():
+    """The B200 arm's last measured line (profiles/r01_bench_line.json, from
+    `python bench.py` on a B200) carries every key the bench contract and the
+    tier's measurement rules ask for, with self-consistent values."""
+    d = json.load(open(os.path.join(ROOT, "profiles", "r01_bench_line.json")))
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e",
+              "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["warmup"] >= 3 and d["n_gpus"] == 1 and d["config"]["workload"]
+    r = d["roofline"]
+    assert 0.0 < r["frac"] <= 1.0 and abs(r["achieved"] / r["peak"] - r["frac"]) < 1e-9
+    assert r["traffic"] is None or r["traffic"] > 0
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
+    assert d["gpu_launches"] > 0
+    assert not set(d["clocks"]["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
