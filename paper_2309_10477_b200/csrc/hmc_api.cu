@@ -13,6 +13,7 @@
 #include <string>
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <utility>
 #include <vector>
 
@@ -53,27 +54,48 @@ cudaError_t call_stream(int device, cudaStream_t* out) {
     return cudaSuccess;
 }
 
-// The one-call entry points allocate their device buffers from the
-// device's default stream-ordered pool.  With the pool's default release
-// threshold (0) every synchronize hands the memory back to the driver and
-// the next call maps it again -- 10-20 ms for the exact scheme's 150 MB
-// node cache.  Keep freed blocks in the pool instead (once per device).
-std::atomic<unsigned long long> g_pool_kept{0};
+// The one-call entry points allocate their device buffers from a
+// stream-ordered pool PRIVATE to libhmc (one per device, created on first
+// use).  The default pool is left untouched, so torch's caching allocator
+// and every other user of it keep their own release policy.  The private
+// pool keeps up to kPoolKeepBytes of freed blocks across synchronizes --
+// enough for the exact scheme's ~150 MB node cache, whose remapping costs
+// 10-20 ms per call -- and hands anything above that back to the driver, so
+// a one-off multi-GB replay buffer is not held for the life of the process.
+constexpr uint64_t kPoolKeepBytes = 256ull << 20;
 
-cudaError_t keep_pool_memory(int dev) {
-    if (dev < 0 || dev >= 64) return cudaSuccess;
-    const unsigned long long bit = 1ULL << dev;
-    if (g_pool_kept.load() & bit) return cudaSuccess;
-    cudaMemPool_t pool;
-    cudaError_t e = cudaDeviceGetDefaultMemPool(&pool, dev);
-    if (e != cudaSuccess) return e;
-    uint64_t keep = ~0ULL;
-    e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    if (e == cudaSuccess) g_pool_kept.fetch_or(bit);
-    return e;
+namespace {
+std::mutex g_pool_mu;
+std::vector<cudaMemPool_t> g_pools;  // by device ordinal
+}  // namespace
+
+cudaError_t pool_alloc(int dev, void** p, size_t bytes, cudaStream_t s) {
+    if (dev < 0 || dev >= 1024) return cudaErrorInvalidDevice;
+    cudaMemPool_t pool = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        if ((size_t)dev >= g_pools.size()) g_pools.resize((size_t)dev + 1, nullptr);
+        if (!g_pools[dev]) {
+            cudaMemPoolProps props{};
+            props.allocType = cudaMemAllocationTypePinned;
+            props.handleTypes = cudaMemHandleTypeNone;
+            props.location.type = cudaMemLocationTypeDevice;
+            props.location.id = dev;
+            cudaMemPool_t created = nullptr;
+            cudaError_t e = cudaMemPoolCreate(&created, &props);
+            if (e != cudaSuccess) return e;
+            uint64_t keep = kPoolKeepBytes;
+            e = cudaMemPoolSetAttribute(created, cudaMemPoolAttrReleaseThreshold, &keep);
+            if (e != cudaSuccess) {
+                cudaMemPoolDestroy(created);
+                return e;
+            }
+            g_pools[dev] = created;
+        }
+        pool = g_pools[dev];
+    }
+    return cudaMallocFromPoolAsync(p, bytes, pool, s);
 }
-
-
 
 // workspace bytes of the bridge tables (S nodes, n_steps + 1 steps, both precisions)
 size_t bridge_bytes(int S, int n_steps) {
@@ -200,8 +222,8 @@ int prepare(const hmc_model* m, const hmc_product* pr, const hmc_sim* sim, Prepa
         return fail(HMC_E_INVALID, "unknown sampler");
     if (sim->precision != HMC_PREC_FP32 && sim->precision != HMC_PREC_FP64)
         return fail(HMC_E_INVALID, "unknown precision");
-    if (sim->n_steps < 1 || sim->n_runs < 1 || sim->n_runs > 65535 || sim->n_paths < 1)
-        return fail(HMC_E_INVALID, "need n_steps >= 1, 1 <= n_runs <= 65535, n_paths >= 1");
+    if (sim->n_steps < 1 || sim->n_runs < 1 || sim->n_paths < 1)
+        return fail(HMC_E_INVALID, "need n_steps >= 1, n_runs >= 1, n_paths >= 1");
     if (sim->path_lo < 0 || sim->path_hi > sim->n_paths || sim->path_lo >= sim->path_hi)
         return fail(HMC_E_INVALID, "path slice must satisfy 0 <= path_lo < path_hi <= n_paths");
     if (sim->path_lo % HMC_CHUNK != 0) return fail(HMC_E_INVALID, "path_lo must be a multiple of HMC_CHUNK");
@@ -353,9 +375,14 @@ __global__ void __launch_bounds__(kRunThreads) chunks_to_runs_kernel(const doubl
 
 cudaError_t launch_tiles_to_chunks(const double* d_tiles, long long n_tiles, int n_runs,
                                    double* d_chunks, long long n_chunks, cudaStream_t s) {
-    tiles_to_chunks_kernel<<<dim3((unsigned)n_chunks, (unsigned)n_runs), 32, 0, s>>>(
-        d_tiles, n_tiles, d_chunks, n_chunks);
-    return cudaGetLastError();
+    for (int r0 = 0; r0 < n_runs; r0 += kMaxRunsPerLaunch) {
+        const int nb = min(kMaxRunsPerLaunch, n_runs - r0);
+        tiles_to_chunks_kernel<<<dim3((unsigned)n_chunks, (unsigned)nb), 32, 0, s>>>(
+            d_tiles + (size_t)r0 * n_tiles * kNW, n_tiles, d_chunks + (size_t)r0 * n_chunks * kNW, n_chunks);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 __global__ void philox_kat_kernel(const uint4* __restrict__ ctr, uint4* __restrict__ out, int n) {
@@ -519,14 +546,13 @@ int hmc_greeks(const hmc_model* model, const hmc_product* product, const hmc_sim
     if (rc) return rc;
     const DeviceGuard keep_device;
     HMC_CK(cudaSetDevice(device));
-    HMC_CK(keep_pool_memory(device));
     cudaStream_t s;
     HMC_CK(call_stream(device, &s));
     const size_t work = (size_t)hmc_workspace_bytes(&sim);
     const size_t chunk_bytes = (size_t)sim.n_runs * P.n_chunks * HMC_NW * sizeof(double);
     const size_t out_bytes = (size_t)sim.n_runs * HMC_NW * sizeof(double);
     char* buf = nullptr;
-    cudaError_t e = cudaMallocAsync((void**)&buf, work + align_up(chunk_bytes) + out_bytes, s);
+    cudaError_t e = pool_alloc(device, (void**)&buf, work + align_up(chunk_bytes) + out_bytes, s);
     if (e == cudaSuccess) {
         double* d_chunks = (double*)(buf + work);
         double* d_out = (double*)(buf + work + align_up(chunk_bytes));
@@ -549,6 +575,9 @@ int hmc_greeks_multi(const hmc_model* model, const hmc_product* product, const h
                      double* h_out, const int32_t* devices, int32_t n_devices) {
     if (!sim_in || !h_out) return fail(HMC_E_INVALID, "sim / h_out is NULL");
     if (!devices || n_devices < 1 || n_devices > 1024) return fail(HMC_E_INVALID, "need 1..1024 devices");
+    if (sim_in->sobol_v_on_device)
+        return fail(HMC_E_INVALID, "hmc_greeks_multi needs a host Sobol direction table "
+                                   "(sobol_v_on_device = 0): a device pointer belongs to one GPU");
     hmc_sim sim = *sim_in;
     sim.path_lo = 0;
     sim.path_hi = sim.n_paths;
@@ -581,7 +610,6 @@ int hmc_greeks_multi(const hmc_model* model, const hmc_product* product, const h
     const int root = devices[0];
     const DeviceGuard keep_device;
     HMC_CK(cudaSetDevice(root));
-    HMC_CK(keep_pool_memory(root));
     cudaStream_t rs;
     HMC_CK(cudaStreamCreateWithFlags(&rs, cudaStreamNonBlocking));
     char* gbuf = nullptr;
@@ -596,12 +624,11 @@ int hmc_greeks_multi(const hmc_model* model, const hmc_product* product, const h
         if (e != cudaSuccess || rc != HMC_OK) break;
         if (q.c_hi <= q.c_lo) continue;
         if ((e = cudaSetDevice(q.dev)) != cudaSuccess) break;
-        if ((e = keep_pool_memory(q.dev)) != cudaSuccess) break;
         if ((e = cudaStreamCreateWithFlags(&q.st, cudaStreamNonBlocking)) != cudaSuccess) break;
         if ((e = cudaEventCreateWithFlags(&q.done, cudaEventDisableTiming)) != cudaSuccess) break;
         const long long nc = q.c_hi - q.c_lo;
         const size_t work = (size_t)hmc_workspace_bytes(&q.sim);
-        if ((e = cudaMallocAsync((void**)&q.buf, work + (size_t)R * nc * row, q.st)) != cudaSuccess) break;
+        if ((e = pool_alloc(q.dev, (void**)&q.buf, work + (size_t)R * nc * row, q.st)) != cudaSuccess) break;
         double* loc = (double*)(q.buf + work);
         rc = hmc_greeks_chunks(model, product, &q.sim, loc, q.buf, q.st);
         if (rc != HMC_OK) break;
@@ -671,14 +698,13 @@ int hmc_discretised_batch_f64(const hmc_model* model, double s0, double T, int32
 
     const DeviceGuard keep_device;
     HMC_CK(cudaSetDevice(device));
-    HMC_CK(keep_pool_memory(device));
     cudaStream_t s;
     HMC_CK(call_stream(device, &s));
     const size_t ub = uniforms ? (size_t)n * 2 * n_steps * sizeof(double) : 0;
     const size_t ob = (size_t)n * 3 * sizeof(double);
     const size_t tb = P.st64.size() * sizeof(StepD);
     char* buf = nullptr;
-    cudaError_t e = cudaMallocAsync((void**)&buf, align_up(ub) + align_up(ob) + tb, s);
+    cudaError_t e = pool_alloc(device, (void**)&buf, align_up(ub) + align_up(ob) + tb, s);
     if (e == cudaSuccess) {
         double* d_u = uniforms ? (double*)buf : nullptr;
         double* d_out = (double*)(buf + align_up(ub));

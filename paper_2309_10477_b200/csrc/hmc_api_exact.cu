@@ -55,7 +55,6 @@ int hmc_exact_runs_f64(const hmc_model* model, double s0, const double* step_tim
 
     const DeviceGuard keep_device;
     HMC_CK(cudaSetDevice(device));
-    HMC_CK(keep_pool_memory(device));
     int dev = 0, sms = 148;
     HMC_CK(cudaGetDevice(&dev));
     HMC_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -74,7 +73,7 @@ int hmc_exact_runs_f64(const hmc_model* model, double s0, const double* step_tim
                          align_up(kb) + align_up(vb) + 256;
     char* buf = nullptr;
     int h_err = 0;
-    cudaError_t ce = cudaMallocAsync((void**)&buf, total, st);
+    cudaError_t ce = pool_alloc(device, (void**)&buf, total, st);
     if (ce == cudaSuccess) {
         size_t off = 0;
         double* d_t = (double*)(buf + off); off += align_up(tb);
@@ -134,8 +133,8 @@ int hmc_exact_greeks_chunks(const hmc_model* model, const hmc_product* product, 
     if (product->right != HMC_CALL && product->right != HMC_PUT) return fail(HMC_E_INVALID, "unknown option right");
     if (sim->want_greeks && product->right != HMC_CALL)
         return fail(HMC_E_UNSUPPORTED, "pathwise Greeks are derived for calls only");
-    if (sim->n_runs < 1 || sim->n_runs > 65535 || sim->n_paths < 1)
-        return fail(HMC_E_INVALID, "need 1 <= n_runs <= 65535 and n_paths >= 1");
+    if (sim->n_runs < 1 || sim->n_paths < 1)
+        return fail(HMC_E_INVALID, "need n_runs >= 1 and n_paths >= 1");
     if (sim->path_lo < 0 || sim->path_hi > sim->n_paths || sim->path_lo >= sim->path_hi ||
         sim->path_lo % HMC_CHUNK != 0)
         return fail(HMC_E_INVALID, "path slice must be chunk aligned within [0, n_paths)");
@@ -194,11 +193,11 @@ int hmc_exact_greeks_chunks(const hmc_model* model, const hmc_product* product, 
     int dev = 0, sms = 148;
     HMC_CK(cudaGetDevice(&dev));
     HMC_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    HMC_CK(keep_pool_memory(dev));
     // runs go through in batches so the observables of all variants stay
     // within ~2 GB of device memory
     const long long per_run = n * 3 * (long long)sizeof(double) * n_var;
-    const long long batch = std::max(1LL, std::min(R, (2LL << 30) / std::max(per_run, 1LL)));
+    const long long batch = std::max(1LL, std::min({R, (long long)hmc::kMaxRunsPerLaunch,
+                                                     (2LL << 30) / std::max(per_run, 1LL)}));
     int grid = 0, variant = 1;
     HMC_CK(hmc::exact_plan(n * batch, sms, &grid, &variant));
     const long long n_tiles = n_tiles_of(n), n_chunks = n_chunks_of(n);
@@ -212,7 +211,7 @@ int hmc_exact_greeks_chunks(const hmc_model* model, const hmc_product* product, 
                          n_var * align_up(ob) + align_up(lb) + 256;
     cudaStream_t st = (cudaStream_t)stream;
     char* buf = nullptr;
-    HMC_CK(cudaMallocAsync((void**)&buf, total, st));
+    HMC_CK(pool_alloc(dev, (void**)&buf, total, st));
     size_t off = 0;
     auto take = [&](size_t bytes) { char* p = buf + off; off += align_up(bytes); return p; };
     double* d_t = (double*)take(tb);

@@ -246,14 +246,13 @@ int hmc_surface(const hmc_model* model, const hmc_surface_spec* spec, const hmc_
     if (rc) return rc;
     const DeviceGuard keep_device;
     HMC_CK(cudaSetDevice(device));
-    HMC_CK(keep_pool_memory(device));
     cudaStream_t st;
     HMC_CK(call_stream(device, &st));
     const size_t acc_bytes = (size_t)hmc_surface_acc_words(spec, sim.n_runs) * sizeof(int64_t);
     const size_t work = (size_t)hmc_surface_workspace_bytes(spec, &sim);
     std::vector<int64_t> h_acc(acc_bytes / sizeof(int64_t));
     char* buf = nullptr;
-    cudaError_t e = cudaMallocAsync((void**)&buf, align_up(acc_bytes) + work, st);
+    cudaError_t e = pool_alloc(device, (void**)&buf, align_up(acc_bytes) + work, st);
     if (e == cudaSuccess) {
         int64_t* d_acc = (int64_t*)buf;
         e = cudaMemsetAsync(d_acc, 0, acc_bytes, st);

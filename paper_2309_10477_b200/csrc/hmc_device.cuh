@@ -15,6 +15,8 @@
 namespace hmc {
 
 constexpr int kTile = HMC_TILE;
+// runs map to gridDim.y; longer run lists go out in launches of this many
+constexpr int kMaxRunsPerLaunch = 65535;
 constexpr int kNQ = HMC_NQ;
 constexpr int kNW = HMC_NW;
 constexpr int kWarps = kTile / 32;
@@ -72,6 +74,7 @@ struct KernelArgs {
     int is_asian, is_call, want_greeks, milstein;
     int sampler;
     int n_runs;
+    int run0;        // global index of the launch's first run (blockIdx.y = run - run0)
     long long n_paths, path_lo, path_hi;
     // root_key(seed) (rng.py:46-47): per-run stream key derivation for both
     // the Philox counter (fp32) and the SplitMix64 stream (fp64)
@@ -131,14 +134,11 @@ __device__ __forceinline__ void mulhilo32(uint32_t a, uint32_t b, uint32_t& hi, 
         : "=r"(hi), "=r"(lo) : "r"(a), "r"(b));
 }
 
-#ifndef HMC_PHILOX_ROUNDS
-#define HMC_PHILOX_ROUNDS 10  // experiments only; the production stream is Philox4x32-10
-#endif
 
 __device__ __forceinline__ uint4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2,
                                                uint32_t c3) {
 #pragma unroll
-    for (int i = 0; i < HMC_PHILOX_ROUNDS; ++i) {
+    for (int i = 0; i < 10; ++i) {
         const uint32_t k0 = kPhiloxK0 + (uint32_t)i * 0x9E3779B9u;
         const uint32_t k1 = kPhiloxK1 + (uint32_t)i * 0xBB67AE85u;
         uint32_t hi0, lo0, hi1, lo1;

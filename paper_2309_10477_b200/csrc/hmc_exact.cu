@@ -23,6 +23,7 @@
 
 #include "hmc_device.cuh"
 #include "hmc_launch.h"
+#include "hmc_ndtri64.cuh"
 
 namespace hmc {
 
@@ -178,39 +179,6 @@ HMC_EXACT_FN cplx phi_node(const PhiPath& P, double a, int* err) {
     return lead * expo * (ser / P.den.re);   // the denominator series has a real argument: real
 }
 
-HMC_EXACT_FN double ndtri_d(double u) {
-    double q, s, num, den, x, e, corr, p, sign;
-    if (u < 1e-300) u = 1e-300;
-    if (u > 1.0 - 1e-16) u = 1.0 - 1e-16;
-    if (0.02425 <= u && u <= 0.97575) {
-        q = u - 0.5;
-        s = q * q;
-        num = ((((-3.969683028665376e+01 * s + 2.209460984245205e+02) * s - 2.759285104469687e+02) * s +
-                1.383577518672690e+02) * s - 3.066479806614716e+01) * s + 2.506628277459239e+00;
-        den = ((((-5.447609879822406e+01 * s + 1.615858368580409e+02) * s - 1.556989798598866e+02) * s +
-                6.680131188771972e+01) * s - 1.328068155288572e+01) * s + 1.0;
-        x = q * num / den;
-    } else {
-        if (u < 0.02425) {
-            p = u;
-            sign = 1.0;
-        } else {
-            p = 1.0 - u;
-            sign = -1.0;
-        }
-        q = sqrt(-2.0 * log(p));
-        num = ((((-7.784894002430293e-03 * q - 3.223964580411365e-01) * q - 2.400758277161838e+00) * q -
-                2.549732539343734e+00) * q + 4.374664141464968e+00) * q + 2.938163982698783e+00;
-        den = (((7.784695709041462e-03 * q + 3.224671290700398e-01) * q + 2.445134137142996e+00) * q +
-               3.754408661907416e+00) * q + 1.0;
-        x = sign * num / den;
-    }
-    e = 0.5 * erfc(-x / sqrt(2.0)) - u;
-    corr = e * 2.5066282746310002 * exp(0.5 * x * x);
-    x -= corr / (1.0 + 0.5 * x * corr);
-    return x;
-}
-
 // Marsaglia-Tsang on the reference stream (_core.pyx:116-136)
 HMC_EXACT_FN double sample_gamma(unsigned long long key, double shape, double scale) {
     double boost = 1.0, alpha = shape;
@@ -223,7 +191,7 @@ HMC_EXACT_FN double sample_gamma(unsigned long long key, double shape, double sc
     const double d = alpha - 1.0 / 3.0;
     const double c = 1.0 / sqrt(9.0 * d);
     while (true) {
-        const double x = ndtri_d(uniform_at(key, ctr));
+        const double x = ndtri_ref(uniform_at(key, ctr));
         double u = uniform_at(key, ctr + 1);
         ctr += 2;
         double v = 1.0 + c * x;
@@ -351,7 +319,7 @@ __device__ double sample_iv(double kappa, double theta, double sigma, double dof
     const double mean = m1, std = sqrt(var);
     if (*err != kErrNone) return 0.0;
     if (std < kDegenerateRelStd * mean) {
-        const double r = mean + std * ndtri_d(u);
+        const double r = mean + std * ndtri_ref(u);
         return r > 0.0 ? r : 0.0;
     }
     const double h = 2.0 * kPi / (mean + kPeriodStds * std);
@@ -492,7 +460,7 @@ __global__ void __launch_bounds__(kExactThreads, MINB) exact_batch_kernel(const 
             const double ek = exp(-e.kappa * dt);
             const double c = e.sigma * e.sigma * (1.0 - ek) / (4.0 * e.kappa);
             const double lam = 4.0 * e.kappa * ek * v / (e.sigma * e.sigma * (1.0 - ek));
-            const double z1 = ndtri_d(u1);
+            const double z1 = ndtri_ref(u1);
             const double g = sample_gamma(derive(gamma_root, (unsigned long long)k), 0.5 * (e.dof - 1.0), 2.0);
             const double shifted = z1 + sqrt(lam);
             const double v_new = c * (g + shifted * shifted);
@@ -500,10 +468,10 @@ __global__ void __launch_bounds__(kExactThreads, MINB) exact_batch_kernel(const 
             if (err != kErrNone) break;
             double int_w2;
             if (point_mass)
-                int_w2 = sqrt(iv) * ndtri_d(u2);
+                int_w2 = sqrt(iv) * ndtri_ref(u2);
             else
                 int_w2 = (v_new - v - e.kappa * e.theta * dt + e.kappa * iv) / e.sigma;
-            const double z3 = ndtri_d(u3);
+            const double z3 = ndtri_ref(u3);
             double var_ln = (1.0 - e.rho * e.rho) * iv;
             if (var_ln < 0.0) var_ln = 0.0;
             ln_s = ln_s + e.r * dt - 0.5 * iv + e.rho * int_w2 + sqrt(var_ln) * z3;

@@ -147,16 +147,11 @@ template <int FIX, bool GREEKS, int SAMPLER>
 __global__ void HMC_BOUNDS fast_greeks_kernel(const KernelArgs a,
                                                             double* __restrict__ tiles,
                                                             long long n_tiles) {
-    const int run = blockIdx.y;
+    const int run = a.run0 + (int)blockIdx.y;
     const long long path = a.path_lo + (long long)blockIdx.x * kTile + threadIdx.x;
     const bool live = path < a.path_hi;
     const long long p = live ? path : a.path_lo;
 
-#ifdef HMC_SMEM_PAD
-    // experiments: cap resident blocks per SM through shared memory
-    __shared__ volatile char occupancy_pad[HMC_SMEM_PAD];
-    if (threadIdx.x == 0) occupancy_pad[0] = 0;
-#endif
     PathState32 st;
     st.v0 = a.f_v0;
     st.vb = make_float2(a.f_vu, a.f_vd);
@@ -288,13 +283,20 @@ cudaError_t launch_given_normals(const KernelArgs& a, const float2* d_z, long lo
 
 cudaError_t launch_fast_greeks(const KernelArgs& a, double* d_tiles, long long n_tiles,
                                cudaStream_t s) {
-    dim3 grid((unsigned)n_tiles, (unsigned)a.n_runs);
-    switch (a.fix_mode) {
-        case kFixLast: launch_greeks_flag<kFixLast>(a, d_tiles, n_tiles, grid, s); break;
-        case kFixEvery: launch_greeks_flag<kFixEvery>(a, d_tiles, n_tiles, grid, s); break;
-        default: launch_greeks_flag<kFixTable>(a, d_tiles, n_tiles, grid, s); break;
+    // runs map to gridDim.y (<= 65535 per launch): batches carry run0
+    for (int r0 = 0; r0 < a.n_runs; r0 += kMaxRunsPerLaunch) {
+        KernelArgs b = a;
+        b.run0 = r0;
+        dim3 grid((unsigned)n_tiles, (unsigned)min(kMaxRunsPerLaunch, a.n_runs - r0));
+        switch (a.fix_mode) {
+            case kFixLast: launch_greeks_flag<kFixLast>(b, d_tiles, n_tiles, grid, s); break;
+            case kFixEvery: launch_greeks_flag<kFixEvery>(b, d_tiles, n_tiles, grid, s); break;
+            default: launch_greeks_flag<kFixTable>(b, d_tiles, n_tiles, grid, s); break;
+        }
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
     }
-    return cudaGetLastError();
+    return cudaSuccess;
 }
 
 }  // namespace hmc

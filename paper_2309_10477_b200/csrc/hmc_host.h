@@ -54,8 +54,9 @@ struct DeviceGuard {
 // destroying a stream per call costs more than a small job's kernel).
 cudaError_t call_stream(int device, cudaStream_t* out);
 
-// keep freed blocks in the device's default stream-ordered pool (hmc_api.cu)
-cudaError_t keep_pool_memory(int dev);
+// stream-ordered allocation from libhmc's private per-device pool (hmc_api.cu);
+// release with cudaFreeAsync
+cudaError_t pool_alloc(int dev, void** p, size_t bytes, cudaStream_t s);
 
 constexpr size_t kAlign = 256;
 inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }

@@ -126,7 +126,6 @@ __device__ __forceinline__ void surface_checkpoint(const PathState32& st, const 
     const int per_style = kSurfVals * nb;
     unsigned long long* g_euro = gacc + ((size_t)0 * s.n_mats + m) * per_style;
     unsigned long long* g_asian = gacc + ((size_t)1 * s.n_mats + m) * per_style;
-#ifndef HMC_SURF_EXP_NOUPDATE
     if (live) {
         const SurfMat mc = s.mats[m];
         const float E = __ldg(a.steps32 + mc.step).x;       // S0 e^{r T_m}
@@ -143,14 +142,7 @@ __device__ __forceinline__ void surface_checkpoint(const PathState32& st, const 
         surface_update(hist + per_style, g_asian, nb, sK, pow2, s.nK, s, mc.d, Aa, st.Ab.x * inv, st.Ab.y * inv,
                        fmaf(st.Dp, inv, Aa), fmaf(st.Dm, inv, Aa), fmaf(st.T1, inv, -mc.T * Aa), al);
     }
-#else
-    // keep the path computation alive in the timing experiment
-    if (st.A0 + st.Ab.x + st.Ab.y + st.L0 + st.Lb.x + st.Lb.y + st.T1 + st.Dp + st.Dm == 1.2345e-30f) atomicAdd(hist, 1);
-#endif
     __syncthreads();
-#ifdef HMC_SURF_EXP_NOFLUSH
-    if (m >= 0) return;  // timing experiment only: results are wrong
-#endif
     // flush this maturity's block histograms into the run accumulators
     for (int i = threadIdx.x; i < 2 * per_style; i += blockDim.x) {
         const int v = hist[i];
@@ -182,7 +174,7 @@ __global__ void __launch_bounds__(kSurfThreads, kSurfMinBlocks) surface_kernel(c
     int pow2 = 1;
     while (pow2 * 2 <= s.nK) pow2 *= 2;
 
-    const int run = blockIdx.y;
+    const int run = a.run0 + (int)blockIdx.y;
     unsigned long long* gacc = s.acc + (size_t)run * 2 * s.n_mats * kSurfVals * nb;
     const unsigned long long key_run = derive(a.root_key, (unsigned long long)run);
     const uint32_t c2 = (uint32_t)key_run, c3 = (uint32_t)(key_run >> 32);
@@ -263,9 +255,15 @@ cudaError_t launch_surface(const KernelArgs& a, const SurfArgs& s, long long n_t
     auto k = a.sampler == HMC_SAMPLER_SOBOL ? surface_kernel<HMC_SAMPLER_SOBOL> : surface_kernel<HMC_SAMPLER_PSEUDO>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    dim3 grid((unsigned)grid_x, (unsigned)a.n_runs);
-    k<<<grid, kSurfThreads, smem, stream>>>(a, s, n_tiles);
-    return cudaGetLastError();
+    for (int r0 = 0; r0 < a.n_runs; r0 += kMaxRunsPerLaunch) {
+        KernelArgs b = a;
+        b.run0 = r0;
+        dim3 grid((unsigned)grid_x, (unsigned)min(kMaxRunsPerLaunch, a.n_runs - r0));
+        k<<<grid, kSurfThreads, smem, stream>>>(b, s, n_tiles);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 }  // namespace hmc

@@ -69,16 +69,17 @@ _DIRECTIONS_ON_DEVICE: dict = {}
 
 
 def _device_directions(host: np.ndarray, dev):
-    """Sobol direction numbers on the device, uploaded once per (table,
-    device): the tables are immutable (sobol.directions is cached and
-    read-only), so repeated QMC calls skip the 60 KB upload."""
+    """Sobol direction numbers on the device, uploaded once per (dimension,
+    device): the table of a dimension is a fixed function of it
+    (sobol.directions), so repeated QMC calls skip the 60 KB upload.  At
+    most one tensor per (dimension, device) is kept."""
     import torch
-    key = (host.shape, dev.index, id(host))
+    key = (int(host.shape[-1]), dev.index)
     hit = _DIRECTIONS_ON_DEVICE.get(key)
-    if hit is None or hit[0] is not host:
-        hit = (host, torch.from_numpy(np.array(host)).to(dev))
+    if hit is None or hit.shape != host.shape:
+        hit = torch.from_numpy(np.array(host)).to(dev)
         _DIRECTIONS_ON_DEVICE[key] = hit
-    return hit[1]
+    return hit
 
 
 class Job:

@@ -25,10 +25,6 @@ VARIANTS = {
     "s768x1": {"HMC_SURF_THREADS": 768, "HMC_SURF_MINB": 1},
     "s384x2": {"HMC_SURF_THREADS": 384, "HMC_SURF_MINB": 2},
     "s896x1": {"HMC_SURF_THREADS": 896, "HMC_SURF_MINB": 1},
-    # timing experiments (wrong results): where the epilogue time goes
-    "x_noflush": {"HMC_SURF_EXP_NOFLUSH": 1},
-    "x_noupdate": {"HMC_SURF_EXP_NOUPDATE": 1},
-    "x_neither": {"HMC_SURF_EXP_NOFLUSH": 1, "HMC_SURF_EXP_NOUPDATE": 1},
 }
 if os.environ.get("SURF_VARIANTS"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["SURF_VARIANTS"].split(",")}
