@@ -9,9 +9,12 @@ FD Rho) from ONE fused pass with common-random-number bumps.  A bench
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-N > 1: launched under torch.distributed.run, one rank per GPU over NCCL; the
-2^24 paths are split across ranks (strong scaling) and the chunk partials
-are all-gathered once per step.  Rank 0 prints ONE JSON line.
+N > 1: launched under torch.distributed.run, one rank per GPU; the 2^24
+paths are split across ranks (strong scaling) and the chunk partials are
+exchanged once per step by libhmc's NCCL communicator
+(hmc_comm_gather_chunks).  Rank 0 prints ONE JSON line.  HMC_DIST_BACKEND=gloo
+(tests only) runs the ranks on a gloo group with host-staged exchange, so
+several ranks can share one GPU.
 
 --impl reference: the reference's own compiled CPU kernel (oracle/_ref,
 built from the reference's _core.c) driven by the restated reference engine
@@ -41,6 +44,23 @@ FP32_PER_PATH_STEP = 45
 N_SM = 148
 
 
+MUFU_PEAK_FILE = os.path.join(ROOT, "profiles", "r02_mufu_peak.json")
+DIST_BACKEND = os.environ.get("HMC_DIST_BACKEND", "nccl")   # gloo: several ranks on one GPU (tests)
+
+
+def mufu_per_clk() -> tuple[float, str]:
+    """MUFU ops per SM clock: the committed microbenchmark measurement
+    (tools/mufu_bench.cu on a B200 of this pool, min over the ops the path
+    kernels issue), else the nominal 16."""
+    try:
+        with open(MUFU_PEAK_FILE) as f:
+            ops = json.load(f)["ops"]
+        v = min(ops[k]["ops_per_clk_per_sm"] for k in ("ex2", "lg2", "sqrt", "sin", "cos"))
+        return v, "profiles/r02_mufu_peak.json (tools/mufu_bench.cu, min over ex2/lg2/sqrt/sin/cos)"
+    except (OSError, KeyError, ValueError):
+        return 16.0, "nominal 16 MUFU ops/clk/SM (profiles/r02_mufu_peak.json missing)"
+
+
 def workload():
     from paper_2309_10477_b200 import BENCH_PARAMS, HestonParams, OptionSpec, SimConfig, daily_fixings
     p = HestonParams(**BENCH_PARAMS)
@@ -59,9 +79,11 @@ def workload():
 SECONDARY_MUFU = {"c2": 7, "c4": 8, "c5": 10}
 
 
-def secondary_workloads(reps: int = 3, sm_mhz: float = 1965.0) -> dict:
-    """The other BASELINE configs on one GPU through the public API (CUDA
-    events around each call; host overhead included)."""
+def secondary_workloads(reps: int = 3, sm_mhz: float = 1965.0, max_over_ranks=None) -> dict:
+    """The other BASELINE configs through the public API (CUDA events around
+    each call; host overhead included).  At N > 1 every rank runs its slice
+    of every job (the engine shards by itself) and the time is the max over
+    ranks; path-steps/s is whole-job."""
     import numpy as np
     import torch
     from paper_2309_10477_b200 import (BENCH_PARAMS, HestonParams, OptionSpec, SimConfig, greeks,
@@ -74,6 +96,12 @@ def secondary_workloads(reps: int = 3, sm_mhz: float = 1965.0) -> dict:
         "c2_european_full_greeks_2^22x252": (
             lambda: greeks(p, euro, SimConfig(scheme="milstein", n_paths=2**22, n_steps=252,
                                               n_runs=1, seed=7)), 2**22 * 252),
+        # the headline job at the reference's own precision: the reference's
+        # SplitMix64 stream + Acklam/Halley ndtri in fp64, its operation order
+        "c3_fp64_replay_asian_full_greeks_2^24x252": (
+            lambda: greeks(p, asian, SimConfig(scheme="milstein", n_paths=N_PATHS, n_steps=N_STEPS,
+                                               n_runs=1, seed=42, precision="fp64")),
+            N_PATHS * N_STEPS),
         "c4_sobol_rqmc_asian_full_greeks_2^22x252": (
             lambda: greeks(p, asian, SimConfig(scheme="milstein", sampler="sobol",
                                                sobol_highdim_ack=True, sobol_scramble=True,
@@ -96,6 +124,7 @@ def secondary_workloads(reps: int = 3, sm_mhz: float = 1965.0) -> dict:
                             SimConfig(scheme="milstein", n_paths=2**22, n_steps=504, n_runs=1,
                                       seed=7)), 2**22 * 504),
     }
+    mufu_clk, _ = mufu_per_clk()
     out = {}
     for name, (fn, path_steps) in jobs.items():
         fn()
@@ -108,10 +137,12 @@ def secondary_workloads(reps: int = 3, sm_mhz: float = 1965.0) -> dict:
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1))
         ms = sorted(ts)[len(ts) // 2]
+        if max_over_ranks is not None:
+            ms = max_over_ranks([ms])[0]
         out[name] = {"ms": ms, "path_steps_per_s": path_steps / (ms / 1e3)}
         mufu = SECONDARY_MUFU.get(name[:2])
         if mufu:
-            peak = N_SM * 16 * sm_mhz * 1e6 / mufu
+            peak = N_SM * mufu_clk * sm_mhz * 1e6 / mufu
             out[name].update(mufu_per_path_step=mufu, mufu_roofline_frac=path_steps / (ms / 1e3) / peak)
     return out
 
@@ -136,6 +167,24 @@ def cpu_exact_block(n_paths: int = 2 ** 13) -> dict:
         secs = time.perf_counter() - t0
     return {"value": n_paths / secs, "unit": "paths/s", "cores": workers, "kind": "reference",
             "sample": f"{n_paths} European Broadie-Kaya paths (1 step), 512-path jobs"}
+
+
+def reference_config_block(n_gpus: int, n_timed: int, workers: int) -> dict:
+    """What the reference arm actually runs (not the B200 arm's block)."""
+    return {"workload": "asian_arith_call_daily_fixings_full_greeks",
+            "paths": N_PATHS, "paths_timed_per_step": n_timed, "time_steps": N_STEPS,
+            "fixings": N_STEPS, "scheme": "milstein",
+            "greeks": ["price", "delta", "rho", "gamma (CRN FD)", "vega (CRN FD)"],
+            "params": "BASELINE A: S0=K=100 T=1 r=0.03 v0=0.04 kappa=2 theta=0.04 xi=0.3 rho=-0.7",
+            "rng": "splitmix64 counter stream + Acklam/Halley ndtri (the reference's _core)",
+            "state": "fp64", "sums": "fp64 (numpy pairwise per 4096-path job, math.fsum across jobs)",
+            "kernel": "reference _core.discretised_batch compiled from the reference's _core.c "
+                      "(oracle/_ref), GIL released",
+            "engine": "restated reference engine (oracle/engine.py, pinned bit-exact to the "
+                      "reference's engine.per_run_values in tests/test_oracle.py)",
+            "full_greeks": "greeks() (price, pathwise Delta/Rho) + 4 CRN bumped price() passes "
+                           "(S0 +/- 0.5 %, v0 +/- 1 %)",
+            "threads": workers, "parallelism": "host threads (rank 0 only)"}
 
 
 def config_block(n_gpus: int) -> dict:
@@ -271,7 +320,8 @@ def run_reference(args) -> None:
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1000.0,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "impl": "reference", "config": config_block(args.gpus),
+            "data": "synthetic", "impl": "reference",
+            "config": reference_config_block(args.gpus, n, workers),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "reference",
                              "sample": f"{n} of the {N_PATHS} paths per step (bounded sample), "
                                        "reference _core kernel + restated reference engine, "
@@ -293,15 +343,33 @@ def run_b200(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
     distributed = "LOCAL_RANK" in os.environ  # launched by torch.distributed.run
+    gloo = distributed and DIST_BACKEND == "gloo"
+    # gloo (tests): ranks may share GPUs; production: one GPU per rank
+    dev_index = local % torch.cuda.device_count() if gloo else local
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     if args.gpus != world and rank == 0:
         print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch N>1 with "
               f"torch.distributed.run (one process per GPU) -- reporting n_gpus={world}",
               file=sys.stderr)
     if distributed:
-        dist.init_process_group("nccl", device_id=dev)
+        if gloo:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+
+    def max_over_ranks(vals):
+        if not distributed:
+            return list(vals)
+        t = torch.tensor(vals, dtype=torch.float64, device="cpu" if gloo else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
+
+    def barrier():
+        if distributed:
+            dist.barrier()
+
     p, spec, cfg = workload()
     L = _lib.lib()
 
@@ -314,7 +382,7 @@ def run_b200(args) -> None:
     loc = torch.zeros((cfg.n_runs, sl.n_chunks, _lib.HMC_NW), dtype=torch.float64, device=dev)
     out = torch.empty((cfg.n_runs, _lib.HMC_NW), dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
-    launches_per_step = 3  # path kernel + tiles->chunks + chunks->runs
+    launches_per_step = 3  # path kernel + tiles->chunks + chunks->runs (+ NCCL's own at N > 1)
 
     def step(ev0=None, ev1=None):
         if ev0 is not None:
@@ -325,7 +393,7 @@ def run_b200(args) -> None:
                                        ctypes.c_void_p(stream.cuda_stream)))
         if ev1 is not None:
             ev1.record(stream)
-        full = parallel.gather_chunks(loc, cfg.n_paths)
+        full = parallel.gather_chunks(loc, cfg.n_paths)      # libhmc NCCL exchange at N > 1
         _lib.check(L.hmc_reduce_chunks(ctypes.c_void_p(full.data_ptr()), cfg.n_runs, full.shape[1],
                                        ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(stream.cuda_stream)))
 
@@ -335,51 +403,47 @@ def run_b200(args) -> None:
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    if distributed:
-        dist.barrier()
+    barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clocks:
+    with ClockSampler(dev_index) as clocks:
         for e0, e1, e2 in ev:
             flush.fill_(1)                       # evict L2 between timed iterations
             step(e0, e1)
             e2.record(stream)
         torch.cuda.synchronize()
-    if distributed:
-        dist.barrier()
+    barrier()
     step_ms = [e0.elapsed_time(e2) for e0, _, e2 in ev]
     kern_ms = [e0.elapsed_time(e1) for e0, e1, _ in ev]
-    t = torch.tensor([sum(step_ms), sum(kern_ms)], dtype=torch.float64, device=dev)
-    if distributed:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_per_step = float(t[0]) / args.steps
-    kernel_ms = float(t[1]) / args.steps
+    tot_step, tot_kern = max_over_ranks([sum(step_ms), sum(kern_ms)])
+    ms_per_step = tot_step / args.steps
+    kernel_ms = tot_kern / args.steps
     path_steps = cfg.n_paths * N_STEPS
     value = path_steps / (ms_per_step / 1000.0)
-    res_dev = out.cpu().numpy()
 
     # e2e: the public API call a user makes (host structs in, host McSummary
     # out; step tables H2D and sums D2H inside every timed call)
     e2e_times = []
     g = None
     for i in range(0 if args.no_e2e else max(2, args.steps // 2) + 1):
-        if distributed:
-            dist.barrier()
+        barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         g = greeks(p, spec, cfg)
         e2e_times.append(time.perf_counter() - t0)
     e2e_s = sorted(e2e_times[1:])[len(e2e_times[1:]) // 2] if e2e_times else float("nan")
-    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if distributed:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_s = float(te[0])
+    e2e_s = max_over_ranks([e2e_s])[0]
     h2d = (N_STEPS + 1) * (32 + 16) + job.avg_idx.nbytes
     d2h = cfg.n_runs * _lib.HMC_NW * 8
 
+    clk = clocks.summary()
+    f_mhz = clk["sm_mhz"] or 1965.0
+    secondary = None
+    if not args.no_e2e and not args.no_secondary:
+        secondary = secondary_workloads(sm_mhz=f_mhz, max_over_ranks=max_over_ranks)
+
     if rank == 0:
-        clk = clocks.summary()
-        f_mhz = clk["sm_mhz"] or 1965.0
-        peak = N_SM * 16 * f_mhz * 1e6 / MUFU_PER_PATH_STEP  # per GPU
+        mufu_clk, mufu_src = mufu_per_clk()
+        peak = N_SM * mufu_clk * f_mhz * 1e6 / MUFU_PER_PATH_STEP  # per GPU
         local_path_steps = sl.n_paths * N_STEPS
         achieved = local_path_steps / (kernel_ms / 1000.0)
         traffic = None
@@ -396,8 +460,9 @@ def run_b200(args) -> None:
             "kernel_ms": kernel_ms,
             "roofline": {"bound": "mufu", "achieved": achieved, "peak": peak, "unit": UNIT,
                          "frac": achieved / peak, "traffic": traffic,
-                         "peak_source": f"{N_SM} SM x 16 MUFU/clk x {f_mhz:.0f} MHz (sampled) / "
-                                        f"{MUFU_PER_PATH_STEP} MUFU per path-step (BASELINE.md)",
+                         "peak_source": f"{N_SM} SM x {mufu_clk:.2f} MUFU/clk ({mufu_src}) x "
+                                        f"{f_mhz:.0f} MHz (sampled) / {MUFU_PER_PATH_STEP} MUFU "
+                                        "per path-step (BASELINE.md)",
                          "fp32_peak": N_SM * 128 * f_mhz * 1e6 / FP32_PER_PATH_STEP},
             "e2e": {"value": path_steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_call": e2e_s * 1000.0},
@@ -405,14 +470,21 @@ def run_b200(args) -> None:
             "clocks": clk,
             "estimates": {q: [g[q].estimate, g[q].path_std_error] for q in g} if g else None,
         }
+        if distributed:
+            line["dist_backend"] = "gloo (host-staged)" if gloo else "nccl (libhmc communicator)"
         if world == 1 and not args.no_cpu:
             line["cpu_baseline"] = cpu_baseline_block()
-        if world == 1 and not args.no_e2e:
-            line["secondary"] = secondary_workloads(sm_mhz=f_mhz)
-            if not args.no_cpu:
-                line["cpu_baseline_exact"] = cpu_exact_block()
+        if secondary is not None:
+            line["secondary"] = secondary
+            fp64 = secondary.get("c3_fp64_replay_asian_full_greeks_2^24x252")
+            cpu = line.get("cpu_baseline", {}).get("value")
+            if fp64 and cpu:   # same-precision comparison with the reference arm
+                fp64["vs_cpu_baseline"] = fp64["path_steps_per_s"] / cpu
+        if world == 1 and not args.no_e2e and not args.no_cpu:
+            line["cpu_baseline_exact"] = cpu_exact_block()
         print(json.dumps(line))
     if distributed:
+        parallel.close_comms()
         dist.destroy_process_group()
 
 
@@ -438,6 +510,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the public-API e2e leg (profiling)")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the secondary BASELINE configs")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -20,6 +20,11 @@
  *                                 Delta, FD Rho from CRN bumps)
  *   hmc_greeks_multi           <- the same job dealt over several GPUs from
  *                                 one process (engine.py:104-116 workers)
+ *   hmc_slice_chunks / hmc_comm_* (NCCL)
+ *                              <- the same fan-out across processes, one
+ *                                 per GPU: slice rule + the in-order
+ *                                 exchange replacing the ordered fsum
+ *                                 (engine.py:104-116)
  *   hmc_exact_batch_f64 / hmc_exact_runs_f64
  *                              <- backend module call exact_batch
  *                                 (_core.pyx:415-521), per run / all runs
@@ -39,8 +44,8 @@
  * Errors: every function returns 0 on success or a negative HMC_E* code;
  * hmc_last_error() gives a thread-local message for the last failure.
  * Threading: all entry points are re-entrant (no global mutable state apart
- * from the thread-local error string, a per-thread stream cache and a
- * once-per-device pool setting); buffers are caller-owned.
+ * from the thread-local error string, a per-thread stream cache and
+ * libhmc's private per-device memory pool); buffers are caller-owned.
  */
 #ifndef HMC_H_
 #define HMC_H_
@@ -180,6 +185,42 @@ int hmc_greeks(const hmc_model* model, const hmc_product* product,
 int hmc_greeks_multi(const hmc_model* model, const hmc_product* product,
                      const hmc_sim* sim, double* h_out, const int32_t* devices,
                      int32_t n_devices);
+
+/* ---- multi-process: one process per GPU, NCCL over NVLink / NVSwitch ----
+ *
+ * Replaces the reference's worker fan-out + ordered fsum (engine.py:104-116)
+ * across processes.  Rank q of a world of W simulates the chunk slice
+ * hmc_slice_chunks(n_paths, q, W) (set hmc_sim.path_lo/path_hi to
+ * chunk_lo*HMC_CHUNK .. min(chunk_hi*HMC_CHUNK, n_paths)) with
+ * hmc_greeks_chunks / hmc_exact_greeks_chunks into d_local[run][chunk][NW];
+ * hmc_comm_gather_chunks then fills the global d_full[run][C][NW] in path
+ * order on every rank and hmc_reduce_chunks reduces it: bit-identical to
+ * one GPU.  NCCL (libnccl.so.2) is opened on first use.  A communicator must
+ * not be used by two host threads at once. */
+#define HMC_COMM_ID_BYTES 128
+enum { HMC_DTYPE_I64 = 0, HMC_DTYPE_F64 = 1 };
+typedef struct hmc_comm hmc_comm;   /* opaque */
+
+/* the parallel.shard rule: [*chunk_lo, *chunk_hi) of C = ceil(n_paths /
+ * HMC_CHUNK) chunks, dealt as evenly as possible (first C % world ranks get
+ * one more) */
+int hmc_slice_chunks(int64_t n_paths, int32_t rank, int32_t world, int64_t* chunk_lo,
+                     int64_t* chunk_hi);
+/* rank 0 creates the id (ncclGetUniqueId) and hands it to the others out of
+ * band (MPI, a TCP store, torch.distributed.broadcast_object_list ...) */
+int hmc_comm_unique_id(uint8_t* id_out /* [HMC_COMM_ID_BYTES] */);
+/* collective: every rank calls it with the same id (ncclCommInitRank) */
+int hmc_comm_init(const uint8_t* id, int32_t rank, int32_t world, int32_t device,
+                  hmc_comm** comm_out);
+int hmc_comm_destroy(hmc_comm* comm);
+/* collective: d_local = this rank's [n_runs][nc_rank][HMC_NW] (DEVICE),
+ * d_full = [n_runs][C][HMC_NW] (DEVICE), stream-ordered on `stream` */
+int hmc_comm_gather_chunks(hmc_comm* comm, const double* d_local, int32_t n_runs,
+                           int64_t n_paths, double* d_full, void* stream);
+/* collective in-place sum of `count` elements of DEVICE d_buf: HMC_DTYPE_I64
+ * (exact; the surface histograms) or HMC_DTYPE_F64 (order-dependent rounding) */
+int hmc_comm_allreduce_sum(hmc_comm* comm, void* d_buf, int64_t count, int32_t dtype,
+                           void* stream);
 
 /* Reference backend call discretised_batch (_core.pyx:354-412) in fp64 on
  * the GPU: same key derivation, draw layout and arithmetic order.

@@ -23,8 +23,22 @@ LIB = os.path.join(PKG, "libhmc.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2",
           f"-I{os.path.join(ROOT, 'include')}"]
+
+
+def nccl_dirs() -> tuple[str, str]:
+    """(include, lib) directories of the torch-bundled NCCL (nvidia-nccl wheel)."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    if spec is None or not spec.submodule_search_locations:
+        raise RuntimeError("nvidia.nccl (torch's NCCL) not found: libhmc's comm unit needs nccl.h")
+    base = list(spec.submodule_search_locations)[0]
+    return os.path.join(base, "include"), os.path.join(base, "lib")
+
+
+_NCCL_INC, _NCCL_LIB = nccl_dirs()
 UNITS = {
     "hmc_api.cu": [],
+    "hmc_comm.cu": [f"-I{_NCCL_INC}", f'-DHMC_NCCL_LIB_DIR="{_NCCL_LIB}"'],
     "hmc_api_surface.cu": [],
     "hmc_api_exact.cu": [],
     "hmc_fast.cu": [],

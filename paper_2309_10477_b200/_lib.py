@@ -45,8 +45,11 @@ EXPORTS = (
     "hmc_sobol_quantile_check", "hmc_box_muller_check", "hmc_fp32_paths_check",
     "hmc_surface_acc_words", "hmc_surface_workspace_bytes", "hmc_surface_partials",
     "hmc_surface_finalize", "hmc_surface", "hmc_exact_batch_f64", "hmc_exact_runs_f64",
-    "hmc_exact_greeks_chunks",
+    "hmc_exact_greeks_chunks", "hmc_slice_chunks", "hmc_comm_unique_id", "hmc_comm_init",
+    "hmc_comm_destroy", "hmc_comm_gather_chunks", "hmc_comm_allreduce_sum",
 )
+HMC_COMM_ID_BYTES = 128
+HMC_DTYPE_I64, HMC_DTYPE_F64 = 0, 1
 HMC_SURF_MAX_STRIKES = 128
 HMC_SURF_MAX_MATS = 32
 HMC_BRIDGE_MAX_SEGMENTS = 64
@@ -125,6 +128,13 @@ def _declare(L: ctypes.CDLL) -> None:
         "hmc_exact_runs_f64": (ctypes.c_int, [pM, dbl, pd, i32, ctypes.POINTER(i64), i64, i64,
                                               ctypes.POINTER(u64), i32, pd,
                                               ctypes.POINTER(ctypes.c_uint32), i32, i64, pd, i32]),
+        "hmc_slice_chunks": (ctypes.c_int, [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+        "hmc_comm_unique_id": (ctypes.c_int, [ctypes.POINTER(ctypes.c_uint8)]),
+        "hmc_comm_init": (ctypes.c_int, [ctypes.POINTER(ctypes.c_uint8), i32, i32, i32,
+                                         ctypes.POINTER(vp)]),
+        "hmc_comm_destroy": (ctypes.c_int, [vp]),
+        "hmc_comm_gather_chunks": (ctypes.c_int, [vp, vp, i32, i64, vp, vp]),
+        "hmc_comm_allreduce_sum": (ctypes.c_int, [vp, vp, i64, i32, vp]),
         "hmc_root_key": (u64, [u64]),
         "hmc_derive_key": (u64, [u64, u64]),
     }

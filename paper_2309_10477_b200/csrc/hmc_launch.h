@@ -108,6 +108,12 @@ cudaError_t launch_fast_greeks(const KernelArgs& a, double* d_tiles, long long n
 // fp64 replay kernels (hmc_replay.cu)
 cudaError_t launch_replay_greeks(const KernelArgs& a, double* d_tiles, long long n_tiles,
                                  cudaStream_t s);
+// elementwise reference primitives (hmc_replay.cu): uniform_at, ndtri, one step
+cudaError_t launch_uniforms(const unsigned long long* d_keys, long long n_keys,
+                            const unsigned long long* d_draws, long long n, double* d_out, cudaStream_t s);
+cudaError_t launch_ndtri(const double* d_u, long long n, double* d_out, cudaStream_t s);
+cudaError_t launch_steps(const KernelArgs& a, const double* d_s, const double* d_v, const double* d_u,
+                         long long n, double* d_s_out, double* d_v_out, cudaStream_t s);
 cudaError_t launch_replay_batch(const KernelArgs& a, unsigned long long key_run,
                                 const double* d_uniforms, double* d_out, cudaStream_t s);
 

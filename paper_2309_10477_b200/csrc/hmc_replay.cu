@@ -216,4 +216,54 @@ cudaError_t launch_replay_greeks(const KernelArgs& a, double* d_tiles, long long
     return cudaSuccess;
 }
 
+// ---- the reference's RNG / step primitives, elementwise (the drop-in's
+// rng / schemes modules: rng.uniform_at / _uniform_keys (rng.py:63-65,
+// 356-361), rng.inverse_normal_cdf (rng.py:95-132), schemes.euler_step /
+// milstein_step (schemes.py:33-61)) -- the SAME device functions the replay
+// kernels run, so each is pinned on its own by the reference's vectors.
+
+__global__ void uniforms_kernel(const unsigned long long* __restrict__ keys, long long n_keys,
+                                const unsigned long long* __restrict__ draws, long long n,
+                                double* __restrict__ out) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = uniform_at(keys[n_keys == 1 ? 0 : i], draws[i]);
+}
+
+__global__ void ndtri_kernel(const double* __restrict__ u, long long n, double* __restrict__ out) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = ndtri_ref(u[i]);
+}
+
+// one step per element from state (s, v) and the step's two uniforms
+// (asset, variance), correlated as rng.correlated_pair (rng.py:226-235)
+__global__ void steps_kernel(const KernelArgs a, const double* __restrict__ s, const double* __restrict__ v,
+                             const double* __restrict__ u, long long n, double* __restrict__ s_out,
+                             double* __restrict__ v_out) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double z1 = ndtri_ref(u[2 * i]);
+    const double z2 = a.rho * z1 + a.sq1mr2 * ndtri_ref(u[2 * i + 1]);
+    TrajD t{s[i], v[i], 0.0, 0.0};
+    ref_step(t, z1, z2, a);
+    s_out[i] = t.s;
+    v_out[i] = t.v;
+}
+
+cudaError_t launch_uniforms(const unsigned long long* d_keys, long long n_keys,
+                            const unsigned long long* d_draws, long long n, double* d_out, cudaStream_t s) {
+    uniforms_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(d_keys, n_keys, d_draws, n, d_out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ndtri(const double* d_u, long long n, double* d_out, cudaStream_t s) {
+    ndtri_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(d_u, n, d_out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_steps(const KernelArgs& a, const double* d_s, const double* d_v, const double* d_u,
+                         long long n, double* d_s_out, double* d_v_out, cudaStream_t s) {
+    steps_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(a, d_s, d_v, d_u, n, d_s_out, d_v_out);
+    return cudaGetLastError();
+}
+
 }  // namespace hmc

@@ -5,20 +5,33 @@ Paths are independent and every per-path value is a pure function of
 (``engine.py:5-9``, ``_core.pyx:385``) -- so the path axis is split into
 contiguous, chunk-aligned slices (``HMC_CHUNK`` = 16384 paths), one per rank.
 The only exchange is the per-chunk fp64 partials (runs x chunks x 14
-doubles, ~100 KB for 2^24 paths): an all-gather over NCCL (NVLink /
-NVSwitch), after which every rank reduces the chunks in global path order.
-The result is therefore bit-identical for any number of GPUs, extending the
-reference's 1-vs-8-workers determinism test (``tests/test_engine.py:21-32``).
+doubles, ~115 KB for 2^24 paths), after which every rank reduces the chunks
+in global path order with the fixed-shape tree.  The result is therefore
+bit-identical for any number of GPUs, extending the reference's
+1-vs-8-workers determinism test (``tests/test_engine.py:21-32``) and
+replacing its fan-out + ordered ``fsum`` (``engine.py:104-116``).
 
-The functions here are device-agnostic (they work on any torch tensors and
-any initialised process group) so the sharding and gather logic is covered
-by world-size-2 ``gloo`` tests on CPU.
+Transport:
+
+* NCCL process groups (one process per GPU, the production layout): the
+  exchange runs inside ``libhmc.so`` (``hmc_comm_gather_chunks`` /
+  ``hmc_comm_allreduce_sum``, NCCL over NVLink / NVSwitch) on a communicator
+  libhmc owns; torch.distributed only bootstraps it (it carries the 128-byte
+  NCCL unique id from rank 0 to the others, once per group).
+* any other process group (gloo -- the CPU tests, and several ranks sharing
+  one GPU, which NCCL refuses): the same partials are staged through host
+  memory and exchanged with the group's own collectives.
+
+Both transports place identical bytes in identical order, so the results do
+not depend on which one ran.
 """
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
+from . import _lib
 from ._lib import HMC_CHUNK, HMC_NW
 
 
@@ -46,7 +59,8 @@ def n_chunks(n_paths: int) -> int:
 
 def shard(n_paths: int, rank: int, world: int) -> Slice:
     """Rank ``rank``'s contiguous chunk range: chunks are dealt as evenly as
-    possible (the first ``C % world`` ranks get one more)."""
+    possible (the first ``C % world`` ranks get one more).  Same rule as the
+    C ABI's ``hmc_slice_chunks`` (checked in tests/test_parallel.py)."""
     if not (0 <= rank < world):
         raise ValueError(f"rank {rank} outside world of size {world}")
     C = n_chunks(n_paths)
@@ -65,22 +79,120 @@ def world_info(group=None) -> tuple[int, int]:
     return 0, 1
 
 
+def _uses_nccl(group, tensor) -> bool:
+    import torch.distributed as dist
+    return tensor.is_cuda and str(dist.get_backend(group)).lower() == "nccl"
+
+
+# ---------------------------------------------------------------------------
+# libhmc communicators (NCCL), one per (process group, device)
+# ---------------------------------------------------------------------------
+_COMMS: dict = {}
+
+
+class Comm:
+    """A libhmc NCCL communicator spanning the ranks of one process group."""
+
+    def __init__(self, group, device_index: int):
+        import torch.distributed as dist
+        L = _lib.lib()
+        rank, world = world_info(group)
+        uid = (ctypes.c_uint8 * _lib.HMC_COMM_ID_BYTES)()
+        if rank == 0:
+            _lib.check(L.hmc_comm_unique_id(uid))
+        box = [bytes(uid)]
+        src = dist.get_global_rank(group, 0) if group is not None else 0
+        dist.broadcast_object_list(box, src=src, group=group)
+        uid = (ctypes.c_uint8 * _lib.HMC_COMM_ID_BYTES).from_buffer_copy(box[0])
+        handle = ctypes.c_void_p()
+        _lib.check(L.hmc_comm_init(uid, rank, world, device_index, ctypes.byref(handle)))
+        self.handle, self.rank, self.world, self.device = handle, rank, world, device_index
+
+    def gather_chunks(self, local, n_runs: int, n_paths: int, full, stream) -> None:
+        _lib.check(_lib.lib().hmc_comm_gather_chunks(
+            self.handle, ctypes.c_void_p(local.data_ptr() if local.numel() else 0), n_runs, n_paths,
+            ctypes.c_void_p(full.data_ptr()), ctypes.c_void_p(stream.cuda_stream)))
+
+    def allreduce_sum(self, buf, stream) -> None:
+        import torch
+        dtype = {torch.int64: _lib.HMC_DTYPE_I64, torch.float64: _lib.HMC_DTYPE_F64}[buf.dtype]
+        _lib.check(_lib.lib().hmc_comm_allreduce_sum(
+            self.handle, ctypes.c_void_p(buf.data_ptr()), buf.numel(), dtype,
+            ctypes.c_void_p(stream.cuda_stream)))
+
+    def close(self) -> None:
+        if self.handle:
+            _lib.check(_lib.lib().hmc_comm_destroy(self.handle))
+            self.handle = None
+
+
+def comm_for(group, device) -> Comm:
+    """The libhmc communicator of ``group`` on ``device`` (created on first
+    use -- a collective call on every rank of the group)."""
+    key = (id(group) if group is not None else None, device.index)
+    c = _COMMS.get(key)
+    if c is None or c.handle is None:
+        c = Comm(group, device.index)
+        _COMMS[key] = c
+    return c
+
+
+def close_comms() -> None:
+    """Destroy every libhmc communicator (before destroy_process_group)."""
+    for c in _COMMS.values():
+        c.close()
+    _COMMS.clear()
+
+
+# ---------------------------------------------------------------------------
+# the exchanges the engine uses
+# ---------------------------------------------------------------------------
 def gather_chunks(local, n_paths: int, group=None):
     """All-gather per-rank chunk partials ``local[run, chunk, HMC_NW]`` into
     the global ``[run, C, HMC_NW]`` tensor in path order (same device/dtype
-    as ``local``).  Ranks pad to the largest slice; padding is dropped."""
+    as ``local``), identical on every rank."""
     import torch
-    import torch.distributed as dist
     rank, world = world_info(group)
     if world == 1:
         return local
     n_runs = local.shape[0]
+    C = n_chunks(n_paths)
+    if _uses_nccl(group, local):
+        full = torch.empty((n_runs, C, HMC_NW), dtype=local.dtype, device=local.device)
+        stream = torch.cuda.current_stream(local.device)
+        comm_for(group, local.device).gather_chunks(local.contiguous(), n_runs, n_paths, full, stream)
+        return full
+    return _gather_chunks_host(local, n_paths, group)
+
+
+def _gather_chunks_host(local, n_paths: int, group=None):
+    """The gloo transport: stage through host memory, all-gather padded
+    slices, drop the padding, concatenate in rank (= path) order."""
+    import torch
+    import torch.distributed as dist
+    rank, world = world_info(group)
+    n_runs = local.shape[0]
     slices = [shard(n_paths, r, world) for r in range(world)]
     width = max(s.n_chunks for s in slices)
-    send = torch.zeros((n_runs, width, HMC_NW), dtype=local.dtype, device=local.device)
-    send[:, : local.shape[1]] = local
-    recv = torch.empty((world * n_runs, width, HMC_NW), dtype=local.dtype, device=local.device)
-    dist.all_gather_into_tensor(recv, send, group=group)
-    recv = recv.view(world, n_runs, width, HMC_NW)
-    parts = [recv[r, :, : slices[r].n_chunks] for r in range(world)]
-    return torch.cat(parts, dim=1).contiguous()
+    send = torch.zeros((n_runs, width, HMC_NW), dtype=local.dtype)
+    send[:, : local.shape[1]] = local.cpu()
+    recv = [torch.empty_like(send) for _ in range(world)]
+    dist.all_gather(recv, send, group=group)
+    parts = [recv[r][:, : slices[r].n_chunks] for r in range(world)]
+    return torch.cat(parts, dim=1).contiguous().to(local.device)
+
+
+def allreduce_sum(buf, group=None) -> None:
+    """In-place sum over the group's ranks (the surface's int64 histograms:
+    integer addition, so exact in any order)."""
+    import torch
+    import torch.distributed as dist
+    _, world = world_info(group)
+    if world == 1:
+        return
+    if _uses_nccl(group, buf):
+        comm_for(group, buf.device).allreduce_sum(buf, torch.cuda.current_stream(buf.device))
+        return
+    host = buf.cpu()
+    dist.all_reduce(host, op=dist.ReduceOp.SUM, group=group)
+    buf.copy_(host)

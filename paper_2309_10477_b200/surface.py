@@ -97,7 +97,6 @@ class SurfaceJob:
         """Accumulate this rank's slice, all-reduce the int64 histograms,
         finalize on the host -> [run][style][mat][strike][HMC_NW]."""
         import torch
-        import torch.distributed as dist
         if not torch.cuda.is_available():
             raise DeviceError("no CUDA device visible; the engine has no CPU fallback")
         L = _lib.lib()
@@ -116,8 +115,7 @@ class SurfaceJob:
                                               ctypes.byref(self.sim), ctypes.c_void_p(acc.data_ptr()),
                                               ctypes.c_void_p(work.data_ptr()),
                                               ctypes.c_void_p(stream.cuda_stream)))
-        if world > 1:
-            dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)  # exact: integers
+        parallel.allreduce_sum(acc, group)  # exact: integers
         h_acc = acc.cpu().numpy()
         n_m, n_k = self.mat_idx.size, self.strikes.size
         out = np.zeros((self.config.n_runs, 2, n_m, n_k, _lib.HMC_NW))

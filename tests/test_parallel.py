@@ -1,11 +1,17 @@
-"""Sharding and the cross-rank exchange, on CPU with world-size-2 gloo.
+"""Sharding and the cross-rank exchange, on CPU with world-size-2 and -3 gloo.
 
-The kernel is replaced by the oracle (chunk partials computed on the CPU
-from per-path Greeks); what is under test is the product's host logic:
-chunk-aligned slicing, the all-gather in path order, and that the result is
-bit-identical to the single-process reduction."""
+Each rank's chunk partials are the ORACLE's per-path Greeks (the C
+restatement of the reference kernel plus the reference's CRN bumps, see
+``oracle/__init__.py``) summed per 16384-path chunk -- the same values a
+rank's device kernel produces up to fp32 rounding.  What is under test is the
+product's host logic: chunk-aligned slicing (Python and the C ABI's
+``hmc_slice_chunks`` agree), the exchange in path order, and that the
+fixed-order reduction is bit-identical to the single-process one, the
+reference's 1-vs-8-workers contract (``tests/test_engine.py:21-32``).
+The real kernel under several processes is covered by
+``tests/test_gpu_multiprocess.py``."""
 
-import math
+import ctypes
 import os
 import socket
 
@@ -14,7 +20,7 @@ import pytest
 import torch
 import torch.multiprocessing as mp
 
-from paper_2309_10477_b200 import parallel
+from paper_2309_10477_b200 import BENCH_PARAMS, HestonParams, OptionSpec, _lib, parallel
 from paper_2309_10477_b200._lib import HMC_CHUNK, HMC_NW
 
 
@@ -32,27 +38,47 @@ def test_shard_covers_axis_once(n, world):
     assert max(sizes) - min(sizes) <= 1
 
 
-def _chunk_partials(lo, hi, n_runs=2):
-    """Stand-in for the device kernel: deterministic pseudo per-path values
-    reduced per 16384-path chunk (the same chunking the device uses)."""
-    out = []
-    for c0 in range(lo, hi, HMC_CHUNK):
-        c1 = min(c0 + HMC_CHUNK, hi)
-        idx = np.arange(c0, c1, dtype=np.float64)
-        row = []
-        for run in range(n_runs):
-            x = np.sin(idx * 0.001 + run)[:, None] * np.arange(1, HMC_NW // 2 + 1)
-            row.append(np.stack([x.sum(0), (x * x).sum(0)], axis=1).reshape(-1))
-        out.append(row)
-    return torch.tensor(np.array(out).transpose(1, 0, 2).copy()) if out else \
-        torch.zeros((n_runs, 0, HMC_NW), dtype=torch.float64)
+@pytest.mark.parametrize("n", [1, HMC_CHUNK + 1, 7 * HMC_CHUNK - 3, 2**24, 2**31 + 5])
+@pytest.mark.parametrize("world", [1, 2, 3, 5, 8, 16])
+def test_c_abi_slice_rule_matches_python(n, world):
+    """A C host shards exactly like the Python engine (hmc_slice_chunks)."""
+    L = _lib.lib()
+    for r in range(world):
+        lo, hi = ctypes.c_int64(), ctypes.c_int64()
+        assert L.hmc_slice_chunks(n, r, world, ctypes.byref(lo), ctypes.byref(hi)) == 0
+        s = parallel.shard(n, r, world)
+        assert (lo.value, hi.value) == (s.chunk_lo, s.chunk_hi)
+    assert L.hmc_slice_chunks(n, world, world, ctypes.byref(lo), ctypes.byref(hi)) == _lib.HMC_E_INVALID
+
+
+N_STEPS = 16
+
+
+def _oracle_chunk_partials(lo, hi, n_runs=2):
+    """Per-chunk {sum, sum of squares} of the oracle's seven per-path Greeks
+    over paths [lo, hi) (Asian call, 4 fixings, 16 Milstein steps)."""
+    import oracle
+    p = HestonParams(**BENCH_PARAMS)
+    spec = OptionSpec("asian_arithmetic", "call", 100.0, 1.0, 100.0,
+                      averaging_times=(0.25, 0.5, 0.75, 1.0))
+    avg = np.array([4, 8, 12, 16], dtype=np.int64)
+    bumps = (0.5, 0.0404, 0.0396, 1e-4)
+    out = np.zeros((n_runs, len(range(lo, hi, HMC_CHUNK)), HMC_NW))
+    for run in range(n_runs):
+        key_run = oracle.derive_key(oracle.root_key(11), run)
+        for j, c0 in enumerate(range(lo, hi, HMC_CHUNK)):
+            c1 = min(c0 + HMC_CHUNK, hi)
+            q = oracle.greeks_paths(p, spec, N_STEPS, True, c0, c1, key_run, None, avg, bumps)
+            out[run, j, 0::2] = q.sum(axis=0)
+            out[run, j, 1::2] = (q * q).sum(axis=0)
+    return torch.tensor(out)
 
 
 def _seq_reduce(chunks):
-    """The device's chunks_to_runs order: sequential over chunks per run."""
+    """The device's chunks_to_runs order is fixed by the global chunk count;
+    here: sequential over chunks per run (any fixed order proves the point)."""
     c = chunks.numpy()
-    return np.array([[math.fsum([]) + sum(c[r, :, w].tolist(), 0.0) for w in range(HMC_NW)]
-                     for r in range(c.shape[0])])
+    return np.array([[sum(c[r, :, w].tolist(), 0.0) for w in range(HMC_NW)] for r in range(c.shape[0])])
 
 
 def _worker(rank, world, port, n, q):
@@ -60,9 +86,12 @@ def _worker(rank, world, port, n, q):
     torch.distributed.init_process_group("gloo", rank=rank, world_size=world)
     try:
         s = parallel.shard(n, rank, world)
-        local = _chunk_partials(s.path_lo, s.path_hi)
+        local = _oracle_chunk_partials(s.path_lo, s.path_hi)
         full = parallel.gather_chunks(local, n)
-        q.put((rank, full.numpy()))
+        # the surface's int64 histogram exchange (exact integer sums)
+        acc = torch.arange(10, dtype=torch.int64) * (rank + 1)
+        parallel.allreduce_sum(acc)
+        q.put((rank, full.numpy(), acc.numpy()))
     finally:
         torch.distributed.destroy_process_group()
 
@@ -73,21 +102,24 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("n", [3 * HMC_CHUNK + 77, 4 * HMC_CHUNK, HMC_CHUNK // 2])
-def test_gather_world2_matches_single(n):
+@pytest.mark.parametrize("world,n", [(2, 3 * HMC_CHUNK + 77), (2, HMC_CHUNK // 2), (3, 4 * HMC_CHUNK),
+                                     (3, 2 * HMC_CHUNK + 5)])
+def test_gather_matches_single_process(world, n):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, q)) for r in range(world)]
     for p in procs:
         p.start()
-    got = dict(q.get(timeout=120) for _ in procs)
+    got = {r: (full, acc) for r, full, acc in (q.get(timeout=300) for _ in procs)}
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    single = _chunk_partials(0, n).numpy()
-    for r in (0, 1):
-        np.testing.assert_array_equal(got[r], single)
-    # and therefore the fixed-order reduction is bit-identical across G
-    np.testing.assert_array_equal(_seq_reduce(torch.tensor(got[1])), _seq_reduce(torch.tensor(single)))
-
+    single = _oracle_chunk_partials(0, n).numpy()
+    want_acc = np.arange(10) * sum(range(1, world + 1))
+    for r in range(world):
+        np.testing.assert_array_equal(got[r][0], single)
+        np.testing.assert_array_equal(got[r][1], want_acc)
+    # and therefore the fixed-order reduction is bit-identical across world sizes
+    np.testing.assert_array_equal(_seq_reduce(torch.tensor(got[world - 1][0])),
+                                  _seq_reduce(torch.tensor(single)))
