@@ -34,6 +34,11 @@
  *                                 config 5) from one path set
  *   hmc_sobol_init_directions  <- scipy.stats.qmc.Sobol direction numbers
  *                                 used by rng.sobol_points (rng.py:143-152)
+ *   hmc_uniforms_f64 / hmc_ndtri_f64 / hmc_gamma_f64 / hmc_steps_f64
+ *                              <- rng.uniform_at / inverse_normal_cdf /
+ *                                 gamma_batch and
+ *                                 schemes.euler_step / milstein_step
+ *                                 (rng.py:63-132, schemes.py:33-61)
  *   hmc_root_key / hmc_derive_key
  *                              <- rng.root_key / rng.derive_key (rng.py:46-52)
  *   hmc_philox_check / hmc_box_muller_check / hmc_sobol_quantile_check /
@@ -359,6 +364,32 @@ int hmc_sobol_quantile_check(const uint32_t* x, int32_t n, int32_t scrambled, fl
 
 /* Key derivation of the reference RNG (rng.py:46-52), for hosts that
  * build key_run for hmc_discretised_batch_f64. */
+/* The reference's random-number and step primitives, elementwise on the
+ * device -- the same device functions the fp64 replay kernels run (built
+ * with -fmad=false).  All buffers HOST, synchronous.  They serve the
+ * drop-in's rng / schemes modules:
+ *   hmc_uniforms_f64  <- rng.uniform_at / uniforms_at / _uniform_keys
+ *                        (rng.py:63-74, 356-361): out[i] = draw draws[i] of
+ *                        the stream keys[n_keys == 1 ? 0 : i]
+ *   hmc_ndtri_f64     <- rng.inverse_normal_cdf (rng.py:95-132; Acklam +
+ *                        one Halley step, _core.pyx:75-109)
+ *   hmc_steps_f64     <- schemes.euler_step / milstein_step (schemes.py:33-61,
+ *                        _core.pyx:399-404): one full-truncation step of each
+ *                        state (s[i], v[i]) from its two uniforms u[i][0]
+ *                        (asset) and u[i][1] (variance), correlated as
+ *                        rng.correlated_pair (rng.py:226-235) */
+int hmc_uniforms_f64(const uint64_t* keys, int64_t n_keys, const uint64_t* draws, int64_t n,
+                     double* out, int32_t device);
+int hmc_ndtri_f64(const double* u, int64_t n, double* out, int32_t device);
+/* rng.gamma_batch / sample_gamma (rng.py:238-262, 308-343; _core.pyx:116-136):
+ * Marsaglia-Tsang Gamma(shape, scale) from draw start[i] of stream keys[i];
+ * used[i] = draws consumed (the exact kernel's own sampler) */
+int hmc_gamma_f64(const uint64_t* keys, const uint64_t* start, int64_t n, double shape,
+                  double scale, double* out, uint64_t* used, int32_t device);
+int hmc_steps_f64(const hmc_model* model, int32_t milstein, double dt, const double* s,
+                  const double* v, const double* u, int64_t n, double* s_out, double* v_out,
+                  int32_t device);
+
 uint64_t hmc_root_key(uint64_t seed);
 uint64_t hmc_derive_key(uint64_t parent, uint64_t index);
 

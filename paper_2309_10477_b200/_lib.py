@@ -47,6 +47,7 @@ EXPORTS = (
     "hmc_surface_finalize", "hmc_surface", "hmc_exact_batch_f64", "hmc_exact_runs_f64",
     "hmc_exact_greeks_chunks", "hmc_slice_chunks", "hmc_comm_unique_id", "hmc_comm_init",
     "hmc_comm_destroy", "hmc_comm_gather_chunks", "hmc_comm_allreduce_sum",
+    "hmc_uniforms_f64", "hmc_ndtri_f64", "hmc_steps_f64", "hmc_gamma_f64",
 )
 HMC_COMM_ID_BYTES = 128
 HMC_DTYPE_I64, HMC_DTYPE_F64 = 0, 1
@@ -135,6 +136,11 @@ def _declare(L: ctypes.CDLL) -> None:
         "hmc_comm_destroy": (ctypes.c_int, [vp]),
         "hmc_comm_gather_chunks": (ctypes.c_int, [vp, vp, i32, i64, vp, vp]),
         "hmc_comm_allreduce_sum": (ctypes.c_int, [vp, vp, i64, i32, vp]),
+        "hmc_uniforms_f64": (ctypes.c_int, [ctypes.POINTER(u64), i64, ctypes.POINTER(u64), i64, pd, i32]),
+        "hmc_ndtri_f64": (ctypes.c_int, [pd, i64, pd, i32]),
+        "hmc_gamma_f64": (ctypes.c_int, [ctypes.POINTER(u64), ctypes.POINTER(u64), i64, dbl, dbl, pd,
+                                         ctypes.POINTER(u64), i32]),
+        "hmc_steps_f64": (ctypes.c_int, [pM, i32, dbl, pd, pd, pd, i64, pd, pd, i32]),
         "hmc_root_key": (u64, [u64]),
         "hmc_derive_key": (u64, [u64, u64]),
     }

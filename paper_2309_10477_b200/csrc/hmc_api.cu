@@ -723,6 +723,109 @@ int hmc_discretised_batch_f64(const hmc_model* model, double s0, double T, int32
     return HMC_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// device round trip of one elementwise primitive on the per-thread stream:
+// `host_in` (bytes each) -> device, launch, device -> `host_out`
+template <class Launch>
+int elementwise_call(int32_t device, const std::vector<std::pair<const void*, size_t>>& host_in,
+                     const std::vector<std::pair<void*, size_t>>& host_out, Launch launch) {
+    const DeviceGuard keep_device;
+    HMC_CK(cudaSetDevice(device));
+    cudaStream_t s;
+    HMC_CK(call_stream(device, &s));
+    size_t total = 0;
+    for (auto& b : host_in) total += align_up(b.second);
+    for (auto& b : host_out) total += align_up(b.second);
+    char* buf = nullptr;
+    HMC_CK(pool_alloc(device, (void**)&buf, std::max<size_t>(total, 256), s));
+    std::vector<void*> dev;
+    size_t off = 0;
+    cudaError_t e = cudaSuccess;
+    for (auto& b : host_in) {
+        dev.push_back(buf + off);
+        if (e == cudaSuccess && b.second) e = cudaMemcpyAsync(buf + off, b.first, b.second, cudaMemcpyHostToDevice, s);
+        off += align_up(b.second);
+    }
+    for (auto& b : host_out) {
+        dev.push_back(buf + off);
+        off += align_up(b.second);
+    }
+    if (e == cudaSuccess) e = launch(dev, s);
+    for (size_t j = 0; j < host_out.size() && e == cudaSuccess; ++j)
+        if (host_out[j].second)
+            e = cudaMemcpyAsync(host_out[j].first, dev[host_in.size() + j], host_out[j].second,
+                                cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(buf, s);
+    const cudaError_t e2 = cudaStreamSynchronize(s);
+    HMC_CK(e);
+    HMC_CK(e2);
+    return HMC_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int hmc_uniforms_f64(const uint64_t* keys, int64_t n_keys, const uint64_t* draws, int64_t n, double* out,
+                     int32_t device) {
+    if (n < 0 || (n > 0 && (!keys || !draws || !out)) || (n_keys != 1 && n_keys != n))
+        return fail(HMC_E_INVALID, "need keys (1 or n of them), draws[n] and out[n]");
+    if (n == 0) return HMC_OK;
+    const size_t kb = (size_t)n_keys * 8, db = (size_t)n * 8;
+    return elementwise_call(device, {{keys, kb}, {draws, db}}, {{out, db}}, [&](auto& d, cudaStream_t s) {
+        return hmc::launch_uniforms((const unsigned long long*)d[0], n_keys, (const unsigned long long*)d[1], n,
+                                    (double*)d[2], s);
+    });
+}
+
+int hmc_ndtri_f64(const double* u, int64_t n, double* out, int32_t device) {
+    if (n < 0 || (n > 0 && (!u || !out))) return fail(HMC_E_INVALID, "need u[n] and out[n]");
+    if (n == 0) return HMC_OK;
+    const size_t b = (size_t)n * 8;
+    return elementwise_call(device, {{u, b}}, {{out, b}}, [&](auto& d, cudaStream_t s) {
+        return hmc::launch_ndtri((const double*)d[0], n, (double*)d[1], s);
+    });
+}
+
+int hmc_gamma_f64(const uint64_t* keys, const uint64_t* start, int64_t n, double shape, double scale,
+                  double* out, uint64_t* used, int32_t device) {
+    if (!(shape > 0.0) || !(scale > 0.0) || !std::isfinite(shape) || !std::isfinite(scale))
+        return fail(HMC_E_INVALID, "gamma shape and scale must be finite and > 0");
+    if (n < 0 || (n > 0 && (!keys || !start || !out || !used)))
+        return fail(HMC_E_INVALID, "need keys[n], start[n], out[n], used[n]");
+    if (n == 0) return HMC_OK;
+    const size_t b = (size_t)n * 8;
+    return elementwise_call(device, {{keys, b}, {start, b}}, {{out, b}, {used, b}}, [&](auto& d, cudaStream_t s) {
+        return hmc::launch_gamma((const unsigned long long*)d[0], (const unsigned long long*)d[1], n, shape, scale,
+                                 (double*)d[2], (unsigned long long*)d[3], s);
+    });
+}
+
+int hmc_steps_f64(const hmc_model* model, int32_t milstein, double dt, const double* s, const double* v,
+                  const double* u, int64_t n, double* s_out, double* v_out, int32_t device) {
+    int rc = check_model(model);
+    if (rc) return rc;
+    if (!(dt > 0.0) || !std::isfinite(dt)) return fail(HMC_E_INVALID, "dt must be finite and > 0");
+    if (n < 0 || (n > 0 && (!s || !v || !u || !s_out || !v_out)))
+        return fail(HMC_E_INVALID, "need s[n], v[n], u[n][2], s_out[n], v_out[n]");
+    for (int64_t i = 0; i < n; ++i)
+        if (!(v[i] >= 0.0) || !(s[i] > 0.0)) return fail(HMC_E_INVALID, "states need s > 0 and v >= 0");
+    if (n == 0) return HMC_OK;
+    KernelArgs a{};
+    a.kappa = model->kappa; a.theta = model->theta; a.sigma = model->sigma;
+    a.rho = model->rho; a.r = model->r; a.v0 = model->v0;
+    a.dt = dt;
+    a.sq1mr2 = std::sqrt(1.0 - model->rho * model->rho);   // _core.pyx:379, rng.py:235
+    a.milstein = milstein ? 1 : 0;
+    const size_t b = (size_t)n * 8;
+    return elementwise_call(device, {{s, b}, {v, b}, {u, 2 * b}}, {{s_out, b}, {v_out, b}},
+                            [&](auto& d, cudaStream_t st) {
+                                return hmc::launch_steps(a, (const double*)d[0], (const double*)d[1],
+                                                         (const double*)d[2], n, (double*)d[3], (double*)d[4], st);
+                            });
+}
+
 int hmc_philox_check(const uint32_t* ctr, int32_t n, uint32_t* out, int32_t device) {
     if (!ctr || !out || n < 1) return fail(HMC_E_INVALID, "bad philox check arguments");
     const DeviceGuard keep_device;

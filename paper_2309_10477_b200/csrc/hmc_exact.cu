@@ -179,14 +179,16 @@ HMC_EXACT_FN cplx phi_node(const PhiPath& P, double a, int* err) {
     return lead * expo * (ser / P.den.re);   // the denominator series has a real argument: real
 }
 
-// Marsaglia-Tsang on the reference stream (_core.pyx:116-136)
-HMC_EXACT_FN double sample_gamma(unsigned long long key, double shape, double scale) {
+// Marsaglia-Tsang on the reference stream (_core.pyx:116-136), from draw
+// ctr0 of the stream; *used = draws consumed
+HMC_EXACT_FN double sample_gamma_from(unsigned long long key, unsigned long long ctr0, double shape,
+                                      double scale, unsigned long long* used) {
     double boost = 1.0, alpha = shape;
-    unsigned long long ctr = 0;
+    unsigned long long ctr = ctr0;
     if (alpha < 1.0) {
-        boost = pow(uniform_at(key, 0), 1.0 / alpha);
+        boost = pow(uniform_at(key, ctr), 1.0 / alpha);
         alpha += 1.0;
-        ctr = 1;
+        ctr += 1;
     }
     const double d = alpha - 1.0 / 3.0;
     const double c = 1.0 / sqrt(9.0 * d);
@@ -198,8 +200,16 @@ HMC_EXACT_FN double sample_gamma(unsigned long long key, double shape, double sc
         if (v <= 0.0) continue;
         v = v * v * v;
         if (u < 1e-300) u = 1e-300;
-        if (log(u) < 0.5 * x * x + d - d * v + d * log(v)) return boost * d * v * scale;
+        if (log(u) < 0.5 * x * x + d - d * v + d * log(v)) {
+            *used = ctr - ctr0;
+            return boost * d * v * scale;
+        }
     }
+}
+
+HMC_EXACT_FN double sample_gamma(unsigned long long key, double shape, double scale) {
+    unsigned long long used;
+    return sample_gamma_from(key, 0ULL, shape, scale, &used);
 }
 
 struct NodeCache {
@@ -572,6 +582,24 @@ cudaError_t launch_exact(const ExactArgs& e, int grid, int variant, cudaStream_t
         exact_batch_kernel<kMinBDeep><<<grid, kExactThreads, 0, s>>>(e);
     else
         exact_batch_kernel<kMinBWide><<<grid, kExactThreads, 0, s>>>(e);
+    return cudaGetLastError();
+}
+
+// one Gamma(shape, scale) draw per (key, start draw) -- rng.gamma_batch /
+// sample_gamma (rng.py:238-262, 308-343) on the device
+__global__ void gamma_kernel(const unsigned long long* __restrict__ keys,
+                             const unsigned long long* __restrict__ start, long long n, double shape,
+                             double scale, double* __restrict__ out, unsigned long long* __restrict__ used) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    unsigned long long u = 0;
+    out[i] = sample_gamma_from(keys[i], start[i], shape, scale, &u);
+    used[i] = u;
+}
+
+cudaError_t launch_gamma(const unsigned long long* d_keys, const unsigned long long* d_start, long long n,
+                         double shape, double scale, double* d_out, unsigned long long* d_used, cudaStream_t s) {
+    gamma_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(d_keys, d_start, n, shape, scale, d_out, d_used);
     return cudaGetLastError();
 }
 

@@ -112,6 +112,9 @@ cudaError_t launch_replay_greeks(const KernelArgs& a, double* d_tiles, long long
 cudaError_t launch_uniforms(const unsigned long long* d_keys, long long n_keys,
                             const unsigned long long* d_draws, long long n, double* d_out, cudaStream_t s);
 cudaError_t launch_ndtri(const double* d_u, long long n, double* d_out, cudaStream_t s);
+// Marsaglia-Tsang Gamma on the reference stream (hmc_exact.cu)
+cudaError_t launch_gamma(const unsigned long long* d_keys, const unsigned long long* d_start, long long n,
+                         double shape, double scale, double* d_out, unsigned long long* d_used, cudaStream_t s);
 cudaError_t launch_steps(const KernelArgs& a, const double* d_s, const double* d_v, const double* d_u,
                          long long n, double* d_s_out, double* d_v_out, cudaStream_t s);
 cudaError_t launch_replay_batch(const KernelArgs& a, unsigned long long key_run,

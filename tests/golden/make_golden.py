@@ -16,6 +16,8 @@ Outputs
                        reference's CRN finite differences on bumped inputs
   rng_cases.json       key derivation, uniform draws, inverse normal
   sobol_points.npz     rng.sobol_points rows
+  primitive_cases.json rng.gamma_batch / sample_gamma, schemes.euler_step /
+                       milstein_step on fixed inputs
   stats_golden.json    (--stats) large-N reference statistics with per-path
                        SE: Milstein Euro/Asian price, Delta, Rho, FD Gamma,
                        FD Vega, FD Rho at BASELINE params, and the
@@ -228,6 +230,54 @@ def rng_cases(hm):
     print("rng_cases.json")
 
 
+def primitive_cases(hm):
+    """Reference rng.gamma_batch / sample_gamma and schemes.euler_step /
+    milstein_step on fixed inputs (the drop-in's device primitives
+    hmc_gamma_f64 / hmc_steps_f64 are checked against these)."""
+    from hestonmc.model import DEFAULT_PARAMS, HestonParams
+    from hestonmc.rng import UniformStream, gamma_batch, sample_gamma, stream_key
+    from hestonmc.schemes import PathState, euler_step, milstein_step
+    keys = [stream_key(41, i) for i in range(64)]
+    gam = {}
+    for shape, scale in ((0.634, 2.0), (2.0, 2.0), (0.05, 1.0), (7.5, 0.5)):
+        gam[f"{shape}_{scale}"] = [float(x) for x in gamma_batch(np.array(keys, dtype=np.uint64), shape, scale)]
+    # scalar sampler from a stream that already consumed 3 draws
+    st = UniformStream(seed=5, stream_index=2)
+    for _ in range(3):
+        st.next_uniform()
+    g_mid = sample_gamma(st, 0.634, 2.0)
+    after = st.next_uniform()
+
+    class _Fixed(UniformStream):
+        def __init__(self, values):
+            super().__init__(kind="pseudo", seed=0)
+            self._v, self._i = list(values), 0
+
+        def next_uniform(self):
+            u = self._v[self._i % len(self._v)]
+            self._i += 1
+            return u
+
+    rng = np.random.default_rng(7)
+    steps = []
+    for pset in (DEFAULT_PARAMS, BENCH, {**BENCH, "rho": 1.0}, {**BENCH, "theta": 0.001, "sigma": 1.5}):
+        p = HestonParams(**pset)
+        for _ in range(8):
+            s0, v0 = float(rng.uniform(50, 150)), float(rng.choice([0.0, rng.uniform(0, 0.2)]))
+            u = [float(x) for x in rng.random(2)]
+            dt = float(rng.choice([1 / 252, 0.125, 0.5]))
+            e = euler_step(_Fixed(u), p, PathState(s0, v0, 0.0), dt)
+            m = milstein_step(_Fixed(u), p, PathState(s0, v0, 0.0), dt)
+            steps.append({"params": pset, "s": s0, "v": v0, "u": u, "dt": dt,
+                          "euler": [e.s, e.v], "milstein": [m.s, m.v]})
+    out = {"gamma_keys": [str(k) for k in keys], "gamma": gam,
+           "gamma_mid_stream": {"seed": 5, "stream_index": 2, "skip": 3, "value": g_mid, "next_draw": after},
+           "steps": steps}
+    with open(os.path.join(HERE, "primitive_cases.json"), "w") as f:
+        json.dump(out, f, indent=1)
+    print("primitive_cases.json")
+
+
 def sobol_cases(hm):
     from hestonmc.rng import sobol_points
     out = {"d504_0": sobol_points(504, 0, 64), "d504_far": sobol_points(504, 3 * 2**20 + 1, 64),
@@ -322,12 +372,17 @@ def stats_golden(hm, core, n_paths=2**20, seed=42, workers=None):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--stats", action="store_true")
+    ap.add_argument("--only", default=None, help="one fixture group, e.g. primitives")
     args = ap.parse_args()
     hm, core = load_reference()
+    if args.only == "primitives":
+        primitive_cases(hm)
+        return
     replay_cases(hm, core)
     engine_cases(hm)
     rng_cases(hm)
     sobol_cases(hm)
+    primitive_cases(hm)
     exact_cases(hm, core)
     if args.stats:
         stats_golden(hm, core)
