@@ -66,10 +66,6 @@ class TestParsing:
         _, _, merged = parse_config(["surface", "--strikes", "90,100", "--maturities", "0.5,1"])
         assert merged["_strikes"] == [90.0, 100.0] and merged["_maturities"] == [0.5, 1.0]
 
-    def test_reference_stream_points(self):
-        import oracle
-        u = cli._reference_uniforms(7, 16)
-        assert list(u) == list(oracle.uniforms_at(oracle.root_key(7), 0, 16))
 
 
 class TestUsageErrors:
@@ -113,7 +109,10 @@ class TestOutputs:
         lines = out.strip().splitlines()
         assert lines[0] == "quantity," + CSV_HEADER
         names = [ln.split(",")[0] for ln in lines[1:]]
-        assert names == ["price", "delta", "gamma", "vega", "rho", "delta_fd", "rho_fd"]
+        assert names == ["price", "delta", "rho"]          # the reference's rows
+        code, out, err = run(capsys, ["greeks", "--format", "csv", "--full-greeks"] + FAST)
+        names = [ln.split(",")[0] for ln in out.strip().splitlines()[1:]]
+        assert code == 0 and names == ["price", "delta", "gamma", "vega", "rho", "delta_fd", "rho_fd"]
 
     def test_exact_default_scheme(self, capsys):
         # the reference's default invocation: exact scheme, sobol, 256 paths
@@ -150,3 +149,7 @@ class TestOutputs:
         assert code == 0 and lines[0] == CSV_HEADER and len(lines) == 5
         body = pts.read_text().splitlines()
         assert body[0] == "sampler,x,y" and len(body) == 1 + 2 * 1024
+        import oracle   # the pseudo pairs are the reference stream keyed root_key(seed)
+        want = oracle.uniforms_at(oracle.root_key(0), 0, 4)
+        got = [float(v) for ln in body[1:3] for v in ln.split(",")[1:]]
+        assert got == [float(f"{x:.10g}") for x in want]
