@@ -420,9 +420,10 @@ __global__ void sobol_quantile_kernel(const uint32_t* __restrict__ x, int n, flo
                                       float* __restrict__ out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int j = min(i, n - 1);
-    const float ht = half * 9.31322574615478515625e-10f;
-    const float2 z = sobol_normal_u2(x[j], x[n - 1 - j], 2.0f * ht, ht);
-    const float s = sobol_normal_u(x[n - 1 - j], 2.0f * ht, ht);
+    const uint32_t mid = half != 0.0f ? 2u : 0u;           // left-aligned coordinates
+    const uint32_t Xa = (x[j] << 2) | mid, Xb = (x[n - 1 - j] << 2) | mid;
+    const float2 z = sobol_normal_X2(Xa, Xb, f2(1.0f));
+    const float s = sobol_normal_X(Xb, 1.0f);
     if (i < n) out[i] = __float_as_uint(s) == __float_as_uint(z.y) ? kSqrt2f * z.x : __int_as_float(0x7fffffff);
 }
 

@@ -50,6 +50,14 @@ namespace hmc {
 #define HMC_BRIDGE_TABLE_STEPS 32
 #endif
 constexpr int kBridgeTableSteps = HMC_BRIDGE_TABLE_STEPS;
+// steps of the time-ordered Sobol loop unrolled together: the quantiles of
+// later steps overlap the trajectory updates of earlier ones (RQMC Asian
+// 2^22 x 252 Greeks: 1 -> 3.71 ms, 2 -> 3.53, 4 -> 3.43, 8 -> 3.33, 16 -> 3.66)
+#ifndef HMC_SOBOL_UNROLL
+#define HMC_SOBOL_UNROLL 8
+#endif
+#define HMC_PRAGMA(x) _Pragma(#x)
+#define HMC_UNROLL(n) HMC_PRAGMA(unroll n)
 using SobolTables = SobolTablesT<kSobolSteps, kWarps>;
 
 constexpr int kSamplerBridge = 2;  // internal: Sobol with Brownian-bridge ordering
@@ -58,20 +66,21 @@ template <int FIX, bool GREEKS>
 __device__ __forceinline__ void sobol_paths(PathState32& st, int run, long long p, const KernelArgs& a) {
     __shared__ SobolTables tab;
     const SobolLane sl(run, p, a.path_lo + (long long)blockIdx.x * kTile, kWarps, a);
-    const float c1 = kSqrt2f * a.f_sqdt * a.f_log2e;  // sobol_pair returns z / sqrt(2)
-    const float cs = kSqrt2f * a.f_sigma * a.f_sqdt;
+    // the quantile returns k z / sqrt(2): fold the step constants into k so
+    //   .x = sqrt(dt) log2(e) z_a                        (= z1l)
+    //   .y = sigma sqrt(dt) sqrt(1 - rho^2) z_b
+    // and sz2 = sigma sqrt(dt) (rho z_a + sqrt(1 - rho^2) z_b) = .y + z1l sigma rho / log2(e)
+    const float2 k = make_float2(kSqrt2f * a.f_sqdt * a.f_log2e, kSqrt2f * a.f_sigma * a.f_sqdt * a.f_sq1mr2);
+    const float crho = a.f_sigma * a.f_rho / a.f_log2e;
 
 #pragma unroll 1
     for (int k0 = 1; k0 <= a.n_sim; k0 += kSobolSteps) {
         const int m = min(kSobolSteps, a.n_sim - k0 + 1);
         sobol_refill(tab, k0 - 1, m, sl, a);
-#pragma unroll 1
+        HMC_UNROLL(HMC_SOBOL_UNROLL)
         for (int q = 0; q < m; ++q) {
-            float za, zb;
-            sobol_pair(tab, q, sl, za, zb);
-            const float z1l = c1 * za;
-            const float sz2 = cs * fmaf(a.f_rho, za, a.f_sq1mr2 * zb);
-            step<FIX, GREEKS, true>(st, k0 + q, z1l, sz2, a);
+            const float2 z = sobol_pair_scaled(tab, q, sl, k);
+            step<FIX, GREEKS, true>(st, k0 + q, z.x, fmaf(z.x, crho, z.y), a);
         }
     }
 }

@@ -66,86 +66,129 @@ __device__ __forceinline__ void tri_unpack(const uint4 w, float (&fr)[3], float 
     fa[2] = __uint_as_float(((w.y << 14) & 0x007FC000u) | ((w.z << 5) & 0x00003FE0u) | 0x3f800000u);
 }
 
-// Standard-normal quantile of the Sobol coordinate u = (x + half) 2^-30:
-// Giles' single-precision erfinv, z = sqrt(2) erfinv(2u - 1), with 4u(1-u)
-// formed from the distance to the nearer end so the tails keep precision.
-// half = 0 for the reference's unscrambled points (x >= 1 always); half = 1/2
-// for digitally shifted points, where x = 0 can occur.  Returns z / sqrt(2)
-// (callers fold sqrt(2) into their constants); hx = half 2^-29 and
-// ht = half 2^-30 are loop invariants of the caller.
-__device__ __forceinline__ float sobol_normal_u(uint32_t x, float hx, float ht) {
-    const bool hi = x >= (1u << 29);
-    const uint32_t t = hi ? (1u << 30) - x : x;              // min(u, 1-u) 2^30 (-+ half)
-    const int m = (int)(2u * x) - (1 << 30);                // (2u - 1) 2^30 - 2 half
-    const float xs = fmaf((float)m, 9.31322574615478515625e-10f, hx);
-    const float tf = fmaf((float)t, 9.31322574615478515625e-10f, hi ? -ht : ht);
-    // w = -ln(4 tf (1 - tf)) = -ln2 (lg2(tf (1 - tf)) + 2)
-    float w = fmaf(lg2a(tf * (1.0f - tf)), -0.69314718055994530942f, -1.38629436111989061883f);
-    float p;
-    // central branch for every lane; the tail branch (|2u - 1| > 0.9966,
-    // 0.3 % of draws) only in warps where a lane needs it: a uniform vote
-    // instead of a divergent if/else around both polynomials
-    {
-        const float wc = w - 2.5f;
-        p = 2.81022636e-08f;
-        p = fmaf(p, wc, 3.43273939e-07f);
-        p = fmaf(p, wc, -3.5233877e-06f);
-        p = fmaf(p, wc, -4.39150654e-06f);
-        p = fmaf(p, wc, 0.00021858087f);
-        p = fmaf(p, wc, -0.00125372503f);
-        p = fmaf(p, wc, -0.00417768164f);
-        p = fmaf(p, wc, 0.246640727f);
-        p = fmaf(p, wc, 1.50140941f);
-    }
-    if (__any_sync(0xffffffffu, w >= 5.0f)) {
-        const float wt = sqrta(w) - 3.0f;
-        float q = -0.000200214257f;
-        q = fmaf(q, wt, 0.000100950558f);
-        q = fmaf(q, wt, 0.00134934322f);
-        q = fmaf(q, wt, -0.00367342844f);
-        q = fmaf(q, wt, 0.00573950773f);
-        q = fmaf(q, wt, -0.0076224613f);
-        q = fmaf(q, wt, 0.00943887047f);
-        q = fmaf(q, wt, 1.00167406f);
-        q = fmaf(q, wt, 2.83297682f);
-        p = w >= 5.0f ? q : p;
-        // extreme cells (t = min(u, 1 - u) < ~3e-8): Giles' single-precision
-        // erfinv is built for float inputs (w <= ~16); use Acklam's lower-tail
-        // rational (the reference's ndtri, _core.pyx:75-109) on t instead
-        if (__any_sync(0xffffffffu, w >= 16.0f)) {
-            const float qa = sqrta(-1.38629436111989061883f * lg2a(tf));   // sqrt(-2 ln t)
-            const float num = fmaf(fmaf(fmaf(fmaf(fmaf(-7.784894002430293e-03f, qa, -3.223964580411365e-01f), qa,
-                                                 -2.400758277161838e+00f), qa, -2.549732539343734e+00f), qa,
-                                       4.374664141464968e+00f), qa, 2.938163982698783e+00f);
-            const float den = fmaf(fmaf(fmaf(fmaf(7.784695709041462e-03f, qa, 3.224671290700398e-01f), qa,
-                                            2.445134137142996e+00f), qa, 3.754408661907416e+00f), qa, 1.0f);
-            const float z = __fdividef(num, den) * 0.70710678118654752440f;   // lower tail: z < 0
-            if (w >= 16.0f) return hi ? -z : z;
-        }
-    }
-    return p * xs;
+// Standard-normal quantile of a Sobol coordinate, Giles' single-precision
+// erfinv: z = sqrt(2) erfinv(2u - 1).  Coordinates arrive LEFT-ALIGNED:
+// X = x << 2 | mid, u = X 2^-32, with mid = 0 for the reference's
+// unscrambled points (u = x 2^-30, x >= 1) and mid = 2 for digitally
+// shifted points (cell midpoints (x + 1/2) 2^-30, x = 0 possible).  Then
+//   t = min(X, 2^32 - X) = (X ^ m) - m,  m = X >> 31 (arithmetic)
+// is exact integer work (2^32 - X = ~X + 1), tf = t 2^-32 = min(u, 1 - u)
+// keeps full relative precision in both tails, w = -ln(4 tf (1 - tf)) and
+// |2u - 1| = 1 - 2 tf with the sign of 2u - 1 = the top bit of X.
+// Returns k z / sqrt(2): callers fold sqrt(2) and their own scale k > 0 in.
+// The tail polynomial (w >= 5, 0.3 % of draws) runs only in warps where a
+// lane needs it (warp vote), the extreme cells (w >= 16, t < ~3e-8, where
+// Giles' float erfinv is out of range) take Acklam's lower-tail rational
+// (the reference's ndtri, _core.pyx:75-109) on tf.
+constexpr float kTwoM32 = 2.3283064365386962890625e-10f;   // 2^-32
+constexpr float kLn2 = 0.69314718055994530942f;
+
+// min(X, 2^32 - X) 2^-32 = min(u, 1 - u).  umin(X, -X) is at most 2^31 (at
+// u = 1/2), which ptxas 12.9 computes as IABS and then converts as a SIGNED
+// integer (X = 2^31 -> -2^31) even through an explicit cvt.rn.f32.u32; the
+// |.| of the converted value (a free FMUL operand modifier) makes the result
+// exact for every X.
+__device__ __forceinline__ float sobol_tail_frac(uint32_t X) {
+    const uint32_t t = min(X, 0u - X);
+    return fabsf(__int2float_rn((int)t)) * kTwoM32;
 }
 
-constexpr float kSqrt2f = 1.41421356237309504880f;
+__device__ __forceinline__ float sobol_sign(float v, uint32_t X) {   // v with the sign of 2u - 1
+    return __uint_as_float(__float_as_uint(v) ^ (~X & 0x80000000u));
+}
 
-#ifndef HMC_SOBOL_PAIR
-#define HMC_SOBOL_PAIR 1     // both coordinates of a step through one paired (FFMA2) quantile
-#endif
+// Acklam lower tail on tf (z < 0), the extreme cells
+__device__ __forceinline__ float acklam_lower_tail(float tf) {
+    const float qa = sqrta(-1.38629436111989061883f * lg2a(tf));   // sqrt(-2 ln t)
+    const float num = fmaf(fmaf(fmaf(fmaf(fmaf(-7.784894002430293e-03f, qa, -3.223964580411365e-01f), qa,
+                                         -2.400758277161838e+00f), qa, -2.549732539343734e+00f), qa,
+                               4.374664141464968e+00f), qa, 2.938163982698783e+00f);
+    const float den = fmaf(fmaf(fmaf(fmaf(7.784695709041462e-03f, qa, 3.224671290700398e-01f), qa,
+                                    2.445134137142996e+00f), qa, 3.754408661907416e+00f), qa, 1.0f);
+    return __fdividef(num, den) * 0.70710678118654752440f;
+}
 
-// sobol_normal_u on two coordinates at once: the same per-lane arithmetic
-// (bit-identical results) with the float work as paired FADD2/FMUL2/FFMA2
-__device__ __forceinline__ float2 sobol_normal_u2(uint32_t xa, uint32_t xb, float hx, float ht) {
-    const bool ha = xa >= (1u << 29), hb = xb >= (1u << 29);
-    const uint32_t ta = ha ? (1u << 30) - xa : xa, tb = hb ? (1u << 30) - xb : xb;
-    const float2 xs = __ffma2_rn(make_float2((float)((int)(2u * xa) - (1 << 30)), (float)((int)(2u * xb) - (1 << 30))),
-                                 f2(9.31322574615478515625e-10f), f2(hx));
-    const float2 tf = __ffma2_rn(make_float2((float)ta, (float)tb), f2(9.31322574615478515625e-10f),
-                                 make_float2(ha ? -ht : ht, hb ? -ht : ht));
-    const float2 om = __ffma2_rn(tf, f2(-1.0f), f2(1.0f));                  // 1 - tf, one rounding
-    const float2 pr = __fmul2_rn(tf, om);
-    const float2 w = __ffma2_rn(make_float2(lg2a(pr.x), lg2a(pr.y)), f2(-0.69314718055994530942f),
-                                f2(-1.38629436111989061883f));
-    const float2 wc = __fadd2_rn(w, f2(-2.5f));
+__device__ __forceinline__ float giles_central(float wc) {   // wc = w - 2.5
+    float p = 2.81022636e-08f;
+    p = fmaf(p, wc, 3.43273939e-07f);
+    p = fmaf(p, wc, -3.5233877e-06f);
+    p = fmaf(p, wc, -4.39150654e-06f);
+    p = fmaf(p, wc, 0.00021858087f);
+    p = fmaf(p, wc, -0.00125372503f);
+    p = fmaf(p, wc, -0.00417768164f);
+    p = fmaf(p, wc, 0.246640727f);
+    return fmaf(p, wc, 1.50140941f);
+}
+
+__device__ __forceinline__ float giles_tail(float wt) {      // wt = sqrt(w) - 3
+    float q = -0.000200214257f;
+    q = fmaf(q, wt, 0.000100950558f);
+    q = fmaf(q, wt, 0.00134934322f);
+    q = fmaf(q, wt, -0.00367342844f);
+    q = fmaf(q, wt, 0.00573950773f);
+    q = fmaf(q, wt, -0.0076224613f);
+    q = fmaf(q, wt, 0.00943887047f);
+    q = fmaf(q, wt, 1.00167406f);
+    return fmaf(q, wt, 2.83297682f);
+}
+
+// scalar form: k z / sqrt(2) of one left-aligned coordinate
+__device__ __forceinline__ float sobol_normal_X(uint32_t X, float k) {
+    const float tf = sobol_tail_frac(X);
+    const float pr = fmaf(-tf, tf, tf);                                  // tf (1 - tf)
+    const float wc = fmaf(lg2a(pr), -kLn2, -2.0f * kLn2 - 2.5f);         // w - 2.5
+    float p = giles_central(wc);
+    if (__any_sync(0xffffffffu, wc >= 2.5f)) {
+        const float q = giles_tail(sqrta(wc + 2.5f) - 3.0f);
+        p = wc >= 2.5f ? q : p;
+        if (__any_sync(0xffffffffu, wc >= 13.5f)) {
+            const float z = acklam_lower_tail(tf) * k;
+            if (wc >= 13.5f) return sobol_sign(-z, X);
+        }
+    }
+    return p * sobol_sign(fmaf(tf, -2.0f * k, k), X);
+}
+
+// the rare part of sobol_normal_X2 (a lane of the warp has w >= 5): Giles'
+// tail polynomial, and for the extreme cells the scalar path.  (Out of line
+// it would keep the unrolled step loop small, but the call costs more than
+// the instruction-cache misses it saves: RQMC Asian 2^22 x 252, 8-step
+// unroll, 3.51 vs 3.33 ms.)  done: the value is the final result; else it
+// is the corrected polynomial value.
+struct SobolTail {
+    float2 v;   // the final result (done) or the corrected polynomial value
+    bool done;
+};
+
+__device__ __forceinline__ SobolTail sobol_tail2(float2 wc, float2 tf, uint32_t Xa, uint32_t Xb, float2 k, float2 p) {
+    const float2 wt = __fadd2_rn(make_float2(sqrta(wc.x + 2.5f), sqrta(wc.y + 2.5f)), f2(-3.0f));
+    float2 q = f2(-0.000200214257f);
+    q = __ffma2_rn(q, wt, f2(0.000100950558f));
+    q = __ffma2_rn(q, wt, f2(0.00134934322f));
+    q = __ffma2_rn(q, wt, f2(-0.00367342844f));
+    q = __ffma2_rn(q, wt, f2(0.00573950773f));
+    q = __ffma2_rn(q, wt, f2(-0.0076224613f));
+    q = __ffma2_rn(q, wt, f2(0.00943887047f));
+    q = __ffma2_rn(q, wt, f2(1.00167406f));
+    q = __ffma2_rn(q, wt, f2(2.83297682f));
+    p.x = wc.x >= 2.5f ? q.x : p.x;
+    p.y = wc.y >= 2.5f ? q.y : p.y;
+    if (__any_sync(0xffffffffu, fmaxf(wc.x, wc.y) >= 13.5f)) {   // extreme cells: the scalar path
+        const float2 xk = __ffma2_rn(tf, make_float2(-2.0f * k.x, -2.0f * k.y), k);
+        const float2 r = __fmul2_rn(p, make_float2(sobol_sign(xk.x, Xa), sobol_sign(xk.y, Xb)));
+        const float sa = sobol_normal_X(Xa, k.x), sb = sobol_normal_X(Xb, k.y);   // all lanes
+        return {make_float2(wc.x >= 13.5f ? sa : r.x, wc.y >= 13.5f ? sb : r.y), true};
+    }
+    return {p, false};
+}
+
+// both coordinates of a step at once: the same per-lane arithmetic as the
+// scalar form (bit-identical), the float work as paired FFMA2/FMUL2; k is
+// the per-coordinate scale
+__device__ __forceinline__ float2 sobol_normal_X2(uint32_t Xa, uint32_t Xb, float2 k) {
+    const float2 tf = make_float2(sobol_tail_frac(Xa), sobol_tail_frac(Xb));
+    const float2 pr = __ffma2_rn(make_float2(-tf.x, -tf.y), tf, tf);
+    const float2 wc = __ffma2_rn(make_float2(lg2a(pr.x), lg2a(pr.y)), f2(-kLn2), f2(-2.0f * kLn2 - 2.5f));
     float2 p = f2(2.81022636e-08f);
     p = __ffma2_rn(p, wc, f2(3.43273939e-07f));
     p = __ffma2_rn(p, wc, f2(-3.5233877e-06f));
@@ -155,27 +198,16 @@ __device__ __forceinline__ float2 sobol_normal_u2(uint32_t xa, uint32_t xb, floa
     p = __ffma2_rn(p, wc, f2(-0.00417768164f));
     p = __ffma2_rn(p, wc, f2(0.246640727f));
     p = __ffma2_rn(p, wc, f2(1.50140941f));
-    if (__any_sync(0xffffffffu, fmaxf(w.x, w.y) >= 5.0f)) {
-        const float2 wt = __fadd2_rn(make_float2(sqrta(w.x), sqrta(w.y)), f2(-3.0f));
-        float2 q = f2(-0.000200214257f);
-        q = __ffma2_rn(q, wt, f2(0.000100950558f));
-        q = __ffma2_rn(q, wt, f2(0.00134934322f));
-        q = __ffma2_rn(q, wt, f2(-0.00367342844f));
-        q = __ffma2_rn(q, wt, f2(0.00573950773f));
-        q = __ffma2_rn(q, wt, f2(-0.0076224613f));
-        q = __ffma2_rn(q, wt, f2(0.00943887047f));
-        q = __ffma2_rn(q, wt, f2(1.00167406f));
-        q = __ffma2_rn(q, wt, f2(2.83297682f));
-        p.x = w.x >= 5.0f ? q.x : p.x;
-        p.y = w.y >= 5.0f ? q.y : p.y;
-        if (__any_sync(0xffffffffu, fmaxf(w.x, w.y) >= 16.0f)) {   // extreme cells: the scalar path
-            const float2 r = __fmul2_rn(p, xs);
-            const float sa = sobol_normal_u(xa, hx, ht), sb = sobol_normal_u(xb, hx, ht);  // all lanes
-            return make_float2(w.x >= 16.0f ? sa : r.x, w.y >= 16.0f ? sb : r.y);
-        }
+    if (__any_sync(0xffffffffu, fmaxf(wc.x, wc.y) >= 2.5f)) {
+        const SobolTail r = sobol_tail2(wc, tf, Xa, Xb, k, p);
+        if (r.done) return r.v;
+        p = r.v;
     }
-    return __fmul2_rn(p, xs);
+    const float2 xk = __ffma2_rn(tf, make_float2(-2.0f * k.x, -2.0f * k.y), k);   // k |2u - 1|
+    return __fmul2_rn(p, make_float2(sobol_sign(xk.x, Xa), sobol_sign(xk.y, Xb)));
 }
+
+constexpr float kSqrt2f = 1.41421356237309504880f;
 
 
 // The two v0-bumped trajectories run as one float2 pair (.x: v0 + h, .y:

@@ -23,7 +23,10 @@ namespace hmc {
 // then does two LDS.64 + two XORs.  Optional random digital shift
 // (a.sobol_shift) per (run, dimension) for randomised QMC, folded into U.
 // ---------------------------------------------------------------------------
-constexpr int kSobolSteps = 64;  // steps per table refill (128 dimensions)
+#ifndef HMC_SOBOL_STEPS
+#define HMC_SOBOL_STEPS 64
+#endif
+constexpr int kSobolSteps = HMC_SOBOL_STEPS;  // steps per table refill (2 dimensions each)
 
 template <int STEPS, int WARPS>
 struct SobolTablesT {
@@ -39,7 +42,7 @@ struct SobolLane {
     int row;            // this lane's block, relative to B0
     uint32_t jl;        // Gray code of the lane part
     unsigned long long key_run;
-    float hx, ht;       // half 2^-29, half 2^-30 (half = 0.5: cell midpoints of shifted points)
+    uint32_t mid;       // 2: left-aligned coordinates are cell midpoints (digitally shifted points)
 
     // p: this thread's path; p_first: the thread block's first path (its
     // paths are consecutive; a dead lane's row is clamped, its values unused)
@@ -53,9 +56,7 @@ struct SobolLane {
         const uint32_t c = n & 31u;
         jl = c ^ (c >> 1);
         key_run = derive(a.root_key, (unsigned long long)run);
-        const float half = a.sobol_scramble ? 0.5f : 0.0f;
-        hx = half * 1.86264514923095703125e-09f;
-        ht = half * 9.31322574615478515625e-10f;
+        mid = a.sobol_scramble ? 2u : 0u;
     }
 };
 
@@ -80,7 +81,7 @@ __device__ __forceinline__ void sobol_refill(Tab& tab, int q0, int m, const Sobo
         for (int j = 1; j < 32; ++j) x[j] = x[j & (j - 1)] ^ v[__ffs(j) - 1];
         uint32_t* col = reinterpret_cast<uint32_t*>(&tab.T[threadIdx.x >> 1][0]) + (threadIdx.x & 1);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) col[2 * j] = x[j];
+        for (int j = 0; j < 32; ++j) col[2 * j] = x[j] << 2;   // left-aligned (sobol_normal_X)
     }
     // high parts: (dimension, group of rows) per thread; a group's first row
     // from the direction numbers, the others incrementally
@@ -104,13 +105,13 @@ __device__ __forceinline__ void sobol_refill(Tab& tab, int q0, int m, const Sobo
                     u ^= __ldg(V + (__ffs(bits) - 1) * dim + d);
                 g = g2;
             }
-            out[r * 2 * Tab::kSteps] = u ^ sh;
+            out[r * 2 * Tab::kSteps] = ((u ^ sh) << 2) | sl.mid;   // left-aligned, midpoint bit
         }
     }
     __syncthreads();
 }
 
-// the two 30-bit coordinates of pair q of the loaded chunk
+// the two left-aligned coordinates X = x << 2 | mid of pair q of the loaded chunk
 template <class Tab>
 __device__ __forceinline__ uint2 sobol_coords(const Tab& tab, int q, const SobolLane& sl) {
     const uint2 t = tab.T[q][sl.jl];
@@ -118,23 +119,22 @@ __device__ __forceinline__ uint2 sobol_coords(const Tab& tab, int q, const Sobol
     return make_uint2(t.x ^ u.x, t.y ^ u.y);
 }
 
-// the two standard normals (divided by sqrt(2)) of a coordinate pair
-__device__ __forceinline__ void sobol_normals(uint2 x, const SobolLane& sl, float& za, float& zb) {
-#if HMC_SOBOL_PAIR
-    const float2 z = sobol_normal_u2(x.x, x.y, sl.hx, sl.ht);
-    za = z.x;
-    zb = z.y;
-#else
-    za = sobol_normal_u(x.x, sl.hx, sl.ht);
-    zb = sobol_normal_u(x.y, sl.hx, sl.ht);
-#endif
-}
-
 // the two standard normals (divided by sqrt(2)) of pair q of the loaded chunk
 template <class Tab>
 __device__ __forceinline__ void sobol_pair(const Tab& tab, int q, const SobolLane& sl,
                                            float& za, float& zb) {
-    sobol_normals(sobol_coords(tab, q, sl), sl, za, zb);
+    const uint2 X = sobol_coords(tab, q, sl);
+    const float2 z = sobol_normal_X2(X.x, X.y, f2(1.0f));
+    za = z.x;
+    zb = z.y;
+}
+
+// pair q as scaled shocks (k.x z_a, k.y z_b) / sqrt(2): the caller's step
+// constants folded into the quantile's last FFMA
+template <class Tab>
+__device__ __forceinline__ float2 sobol_pair_scaled(const Tab& tab, int q, const SobolLane& sl, float2 k) {
+    const uint2 X = sobol_coords(tab, q, sl);
+    return sobol_normal_X2(X.x, X.y, k);
 }
 
 

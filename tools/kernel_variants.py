@@ -18,11 +18,17 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "paper_2309_10477_b200", "_variants")
 
-VARIANTS = {
-    "base": {},
-    "lb6": {"HMC_MIN_BLOCKS": 6},
-    "lb8": {"HMC_MIN_BLOCKS": 8},
+VARIANT_SETS = {
+    "occupancy": {"base": {}, "lb6": {"HMC_MIN_BLOCKS": 6}, "lb8": {"HMC_MIN_BLOCKS": 8}},
+    # RQMC Sobol driver (time with HMC_VARIANT_SOBOL=1)
+    "sobol": {"u8": {"HMC_SOBOL_UNROLL": 8, "HMC_SOBOL_TAIL_NOINLINE": 0},
+              "u8_lb8": {"HMC_SOBOL_UNROLL": 8, "HMC_SOBOL_TAIL_NOINLINE": 0, "HMC_MIN_BLOCKS": 8},
+              "u8_s32": {"HMC_SOBOL_UNROLL": 8, "HMC_SOBOL_TAIL_NOINLINE": 0, "HMC_SOBOL_STEPS": 32},
+              "u8_s32_lb8": {"HMC_SOBOL_UNROLL": 8, "HMC_SOBOL_TAIL_NOINLINE": 0, "HMC_SOBOL_STEPS": 32,
+                             "HMC_MIN_BLOCKS": 8},
+              "u16": {"HMC_SOBOL_UNROLL": 16, "HMC_SOBOL_TAIL_NOINLINE": 0}},
 }
+VARIANTS = VARIANT_SETS[os.environ.get("HMC_VARIANT_SET", "occupancy")]
 
 
 def build():
