@@ -21,12 +21,10 @@ VDIR = os.path.join(ROOT, "paper_2309_10477_b200", "_variants")
 VARIANT_SETS = {
     "occupancy": {"base": {}, "lb6": {"HMC_MIN_BLOCKS": 6}, "lb8": {"HMC_MIN_BLOCKS": 8}},
     # RQMC Sobol driver (time with HMC_VARIANT_SOBOL=1)
-    "sobol": {"u8": {"HMC_SOBOL_UNROLL": 8, "HMC_SOBOL_TAIL_NOINLINE": 0},
-              "u8_lb8": {"HMC_SOBOL_UNROLL": 8, "HMC_SOBOL_TAIL_NOINLINE": 0, "HMC_MIN_BLOCKS": 8},
-              "u8_s32": {"HMC_SOBOL_UNROLL": 8, "HMC_SOBOL_TAIL_NOINLINE": 0, "HMC_SOBOL_STEPS": 32},
-              "u8_s32_lb8": {"HMC_SOBOL_UNROLL": 8, "HMC_SOBOL_TAIL_NOINLINE": 0, "HMC_SOBOL_STEPS": 32,
-                             "HMC_MIN_BLOCKS": 8},
-              "u16": {"HMC_SOBOL_UNROLL": 16, "HMC_SOBOL_TAIL_NOINLINE": 0}},
+    "sobol": {"u8": {}},
+    # bridge-ordered Sobol (time with HMC_VARIANT_SOBOL=1 HMC_VARIANT_BRIDGE=16)
+    "bridge": {"b1": {}, "b2": {"HMC_BRIDGE_UNROLL": 2}, "b4": {"HMC_BRIDGE_UNROLL": 4},
+               "b8": {"HMC_BRIDGE_UNROLL": 8}},
 }
 VARIANTS = VARIANT_SETS[os.environ.get("HMC_VARIANT_SET", "occupancy")]
 
@@ -53,7 +51,8 @@ if _os.environ.get("HMC_VARIANT_EURO"):
     from paper_2309_10477_b200 import OptionSpec as _OS
     spec = _OS("european", "call", 100.0, 1.0, 100.0)
 if _os.environ.get("HMC_VARIANT_SOBOL"):
-    cfg = _dc.replace(cfg, sampler="sobol", sobol_highdim_ack=True, sobol_scramble=True, n_paths=2**22)
+    cfg = _dc.replace(cfg, sampler="sobol", sobol_highdim_ack=True, sobol_scramble=True, n_paths=2**22,
+                      sobol_bridge=int(_os.environ.get("HMC_VARIANT_BRIDGE", "0")))
 job = engine.Job(p, spec, cfg, True)
 if job.sobol_host is not None:
     import numpy as _np
