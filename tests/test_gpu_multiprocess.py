@@ -156,3 +156,41 @@ def test_bench_torchrun_two_ranks_gloo():
     g = greeks(*bench.workload())
     for q, (est, se) in line["estimates"].items():
         assert est == g[q].estimate and se == g[q].path_std_error, q
+
+
+def _nccl_world1_worker(port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.path.insert(0, ROOT)
+    try:
+        torch.cuda.set_device(0)
+        dev = torch.device("cuda", 0)
+        torch.distributed.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+        from paper_2309_10477_b200 import _lib, parallel
+        comm = parallel.Comm(None, 0)            # bootstrap: unique id over the NCCL group
+        s = torch.cuda.current_stream()
+        n = 3 * CHUNK + 5
+        local = torch.randn((2, 4, _lib.HMC_NW), dtype=torch.float64, device=dev)
+        full = torch.empty_like(local)
+        comm.gather_chunks(local, 2, n, full, s)
+        acc = torch.arange(7, dtype=torch.int64, device=dev)
+        comm.allreduce_sum(acc, s)
+        torch.cuda.synchronize()
+        ok = torch.equal(full, local) and torch.equal(acc.cpu(), torch.arange(7))
+        comm.close()
+        torch.distributed.destroy_process_group()
+        q.put((ok, None))
+    except Exception:  # noqa: BLE001 - reported to the parent
+        import traceback
+        q.put((False, traceback.format_exc()))
+
+
+def test_comm_bootstrap_over_nccl_group():
+    """parallel.Comm's bootstrap (rank 0's NCCL id over a torch NCCL group)
+    and both exchanges, in a world-1 NCCL process group."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_world1_worker, args=(_free_port(), q))
+    p.start()
+    ok, err = q.get(timeout=300)
+    p.join(timeout=60)
+    assert ok, err
