@@ -11,9 +11,11 @@
 // path order on every rank.  hmc_reduce_chunks then reduces it with the
 // fixed-shape tree, so the result is bit-identical for any number of GPUs.
 //
-// The exchange is world grouped ncclBroadcasts (rank q is the root of its own
-// exact-sized slice; no padding), straight into place when n_runs == 1 and
-// through a private scratch + one 2-D copy per rank otherwise.  Payload:
+// The exchange is one ncclAllGather straight into place when every rank
+// holds the same number of chunks and there is one run (the bench job:
+// 1024 chunks over 1/2/4/8 GPUs), else world grouped ncclBroadcasts (rank q
+// the root of its own exact-sized slice; no padding), into place for one run
+// and through a private scratch + one 2-D copy per rank for several.  Payload:
 // n_chunks * n_runs * 112 B (115 KB for the 2^24-path bench job) --
 // latency-bound, a few microseconds over NVSwitch.
 //
@@ -52,6 +54,7 @@ struct NcclApi {
                               cudaStream_t) = nullptr;
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -79,6 +82,7 @@ void load_nccl() {
     g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))sym("ncclCommDestroy");
     g_nccl.Broadcast = (decltype(g_nccl.Broadcast))sym("ncclBroadcast");
     g_nccl.AllReduce = (decltype(g_nccl.AllReduce))sym("ncclAllReduce");
+    g_nccl.AllGather = (decltype(g_nccl.AllGather))sym("ncclAllGather");
     g_nccl.GroupStart = (decltype(g_nccl.GroupStart))sym("ncclGroupStart");
     g_nccl.GroupEnd = (decltype(g_nccl.GroupEnd))sym("ncclGroupEnd");
     g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))sym("ncclGetErrorString");
@@ -180,6 +184,12 @@ int hmc_comm_gather_chunks(hmc_comm* comm, const double* d_local, int32_t n_runs
     cudaStream_t st = (cudaStream_t)stream;
     const DeviceGuard keep_device;
     HMC_CK(cudaSetDevice(comm->device));
+    if (R == 1 && C % comm->world == 0) {
+        // equal slices, rank-major = path order: one all-gather straight into place
+        HMC_NCCL(g_nccl.AllGather(d_local, d_full, (size_t)(C / comm->world) * HMC_NW, ncclDouble, comm->nccl,
+                                  st));
+        return HMC_OK;
+    }
     if (R == 1) {  // slices are contiguous in the global array: broadcast into place
         HMC_NCCL(g_nccl.GroupStart());
         for (int q = 0; q < comm->world; ++q) {

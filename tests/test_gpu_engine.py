@@ -556,3 +556,26 @@ def test_path_standard_error_is_calibrated(bench_params):
     for q in QN:
         ratio = np.std(est[q], ddof=1) / np.mean(se[q])
         assert 0.6 < ratio < 1.45, (q, ratio)
+
+
+class TestManyRuns:
+    """Runs map to gridDim.y; beyond 65 535 they go out in launch batches
+    with a run offset (KernelArgs.run0).  The reference engine has no run
+    limit (engine.py:151); its per-run values are checked at the batch
+    boundary against the oracle's restatement of ``_run_sums``."""
+
+    def test_runs_past_grid_y_limit(self, bench_params, euro_call):
+        cfg = SimConfig(scheme="milstein", n_paths=32, n_steps=4, n_runs=65537, seed=3,
+                        precision="fp64")
+        s = price(bench_params, euro_call, cfg)
+        assert len(s.per_run_values) == 65537
+        for run in (0, 65534, 65535, 65536):
+            want = oe.run_sums(bench_params, euro_call, cfg, run, None, False, "port")[0] / cfg.n_paths
+            assert math.isclose(s.per_run_values[run], want, rel_tol=1e-12), run
+        # fp32 production path: the batch boundary changes nothing either
+        f = greeks(bench_params, euro_call, SimConfig(scheme="milstein", n_paths=32, n_steps=4,
+                                                       n_runs=65537, seed=3))
+        g = greeks(bench_params, euro_call, SimConfig(scheme="milstein", n_paths=32, n_steps=4,
+                                                       n_runs=3, seed=3))
+        assert f["vega"].per_run_values[:3] == g["vega"].per_run_values
+        assert len(set(f["price"].per_run_values[65530:])) == 7

@@ -1,7 +1,7 @@
 """Opcode histogram of the innermost loop(s) of a kernel's SASS (dev tool):
 python tools/sass_loop.py <lib.so> <mangled kernel name> [needle opcode]
-The loop is the smallest backward-branch range that contains the needle
-(default MUFU.LG2)."""
+The loop is the backward-branch range with the most needle instructions
+(default MUFU.LG2), the smallest among equals."""
 import re
 import subprocess
 import sys
@@ -26,8 +26,9 @@ for i, (a, text) in enumerate(ins):
         continue
     lo, hi = addr[tgt], i
     body = [t for _, t in ins[lo:hi + 1]]
-    if any(needle in t for t in body) and (best is None or hi - lo < best[1] - best[0]):
-        best = (lo, hi)
+    hits = sum(needle in t for t in body)
+    if hits and (best is None or (hits, lo - hi) > (best[2], best[0] - best[1])):
+        best = (lo, hi, hits)
 if best is None:
     sys.exit("no loop with " + needle)
 body = [t for _, t in ins[best[0]:best[1] + 1]]
