@@ -58,11 +58,14 @@ cudaError_t call_stream(int device, cudaStream_t* out) {
 // stream-ordered pool PRIVATE to libhmc (one per device, created on first
 // use).  The default pool is left untouched, so torch's caching allocator
 // and every other user of it keep their own release policy.  The private
-// pool keeps up to kPoolKeepBytes of freed blocks across synchronizes --
-// enough for the exact scheme's ~150 MB node cache, whose remapping costs
-// 10-20 ms per call -- and hands anything above that back to the driver, so
-// a one-off multi-GB replay buffer is not held for the life of the process.
-constexpr uint64_t kPoolKeepBytes = 256ull << 20;
+// pool keeps up to kPoolKeepBytes of freed blocks across synchronizes: the
+// exact scheme's node cache (up to ~310 MB: 256 fp64 nodes per resident
+// thread) is re-mapped on every call otherwise -- measured 310 ms per
+// 2^17-path exact price with a 256 MB threshold, 0.8 ms with 1 GiB --
+// while a one-off multi-GB buffer (a caller's replay uniforms) above the
+// threshold goes back to the driver instead of being held for the life of
+// the process.
+constexpr uint64_t kPoolKeepBytes = 1ull << 30;
 
 namespace {
 std::mutex g_pool_mu;
