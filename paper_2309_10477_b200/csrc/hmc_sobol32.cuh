@@ -26,7 +26,7 @@ namespace hmc {
 #ifndef HMC_SOBOL_STEPS
 #define HMC_SOBOL_STEPS 64
 #endif
-constexpr int kSobolSteps = HMC_SOBOL_STEPS;  // steps per table refill (2 dimensions each)
+constexpr int kSobolSteps = HMC_SOBOL_STEPS;  // steps per table refill (2 dimensions each, <= 64)
 
 template <int STEPS, int WARPS>
 struct SobolTablesT {

@@ -21,7 +21,7 @@ VDIR = os.path.join(ROOT, "paper_2309_10477_b200", "_variants")
 VARIANT_SETS = {
     "occupancy": {"base": {}, "lb6": {"HMC_MIN_BLOCKS": 6}, "lb8": {"HMC_MIN_BLOCKS": 8}},
     # RQMC Sobol driver (time with HMC_VARIANT_SOBOL=1)
-    "sobol": {"u8": {}},
+    "sobol": {"u8": {}, "u4": {"HMC_SOBOL_UNROLL": 4}},
     # bridge-ordered Sobol (time with HMC_VARIANT_SOBOL=1 HMC_VARIANT_BRIDGE=16)
     "bridge": {"b1": {}, "b2": {"HMC_BRIDGE_UNROLL": 2}, "b4": {"HMC_BRIDGE_UNROLL": 4},
                "b8": {"HMC_BRIDGE_UNROLL": 8}},
