@@ -191,6 +191,14 @@ void fill_fp32_constants(KernelArgs& a) {
     a.f_rho = (float)a.rho;
     a.f_sq1mr2 = (float)a.sq1mr2;
     a.f_sqdt = (float)std::sqrt(a.dt);
+    {
+        const float sq2 = 1.41421356237309504880f;   // hmc_path32.cuh kSqrt2f
+        a.f_sob_k.x = sq2 * a.f_sqdt * a.f_log2e;
+        a.f_sob_k.y = sq2 * a.f_sigma * a.f_sqdt * a.f_sq1mr2;
+        a.f_sob_k2.x = -2.0f * a.f_sob_k.x;
+        a.f_sob_k2.y = -2.0f * a.f_sob_k.y;
+        a.f_sob_crho = a.f_sigma * a.f_rho / a.f_log2e;
+    }
     a.f_v0 = (float)a.v0;
     a.f_vu = (float)a.v0_up;
     a.f_vd = (float)a.v0_dn;

@@ -161,13 +161,14 @@ int hmc_exact_greeks_chunks(const hmc_model* model, const hmc_product* product, 
     const bool asian = product->style == HMC_STYLE_ASIAN, greeks = sim->want_greeks != 0;
     const double T = product->maturity, r = model->r;
 
-    // model variants simulated on the same streams: base, v0 +- , r +- (Asian)
-    hmc_model var[5] = {*model, *model, *model, *model, *model};
+    // model variants simulated on the same streams: base, v0 +-.  The r +- h_r
+    // underlyings are the base paths rescaled (exact_estimator_kernel): the
+    // base run of an Asian carries sum S_k expm1(+-h_r t_k) as two more columns
+    hmc_model var[3] = {*model, *model, *model};
     var[1].v0 = sim->v0_up;
     var[2].v0 = sim->v0_dn;
-    var[3].r = r + sim->h_r;
-    var[4].r = r - sim->h_r;
-    const int n_var = !greeks ? 1 : (asian ? 5 : 3);
+    const int n_var = greeks ? 3 : 1;
+    const bool rcols = greeks && asian;
 
     // epilogue arguments (hmc_device.cuh greeks_epilogue)
     KernelArgs a{};
@@ -195,7 +196,7 @@ int hmc_exact_greeks_chunks(const hmc_model* model, const hmc_product* product, 
     HMC_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     // runs go through in batches so the observables of all variants stay
     // within ~2 GB of device memory
-    const long long per_run = n * 3 * (long long)sizeof(double) * n_var;
+    const long long per_run = n * (long long)sizeof(double) * (3 * n_var + (rcols ? 2 : 0));
     const long long batch = std::max(1LL, std::min({R, (long long)hmc::kMaxRunsPerLaunch,
                                                      (2LL << 30) / std::max(per_run, 1LL)}));
     int grid = 0, variant = 1;
@@ -206,9 +207,11 @@ int hmc_exact_greeks_chunks(const hmc_model* model, const hmc_product* product, 
     const size_t vb = sob && !sim->sobol_v_on_device ? (size_t)30 * 3 * n_steps * sizeof(uint32_t) : 0;
     const size_t sb = (size_t)hmc::kExactCacheNodes * grid * hmc::kExactThreads * sizeof(double);
     const size_t ob = (size_t)batch * n * 3 * sizeof(double);
+    const size_t ob0 = (size_t)batch * n * (rcols ? 5 : 3) * sizeof(double);
+    const size_t eb = rcols ? ((size_t)n_steps + 1) * 2 * sizeof(double) : 0;
     const size_t lb = (size_t)R * n_tiles * HMC_NW * sizeof(double);
     const size_t total = align_up(tb) + align_up(fb) + align_up(kb) + align_up(vb) + align_up(sb) +
-                         n_var * align_up(ob) + align_up(lb) + 256;
+                         align_up(ob0) + (n_var - 1) * align_up(ob) + align_up(eb) + align_up(lb) + 256;
     cudaStream_t st = (cudaStream_t)stream;
     char* buf = nullptr;
     HMC_CK(pool_alloc(dev, (void**)&buf, total, st));
@@ -219,8 +222,14 @@ int hmc_exact_greeks_chunks(const hmc_model* model, const hmc_product* product, 
     unsigned long long* d_k = (unsigned long long*)take(kb);
     uint32_t* d_v = vb ? (uint32_t*)take(vb) : nullptr;
     double* d_s = (double*)take(sb);
-    double* d_obs[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
-    for (int v = 0; v < n_var; ++v) d_obs[v] = (double*)take(ob);
+    double* d_obs[3] = {nullptr, nullptr, nullptr};
+    for (int v = 0; v < n_var; ++v) d_obs[v] = (double*)take(v == 0 ? ob0 : ob);
+    double* d_e = eb ? (double*)take(eb) : nullptr;
+    std::vector<double> em(rcols ? 2 * ((size_t)n_steps + 1) : 0);
+    for (size_t k = 0; rcols && k <= (size_t)n_steps; ++k) {
+        em[2 * k] = std::expm1(sim->h_r * step_times[k]);
+        em[2 * k + 1] = std::expm1(-sim->h_r * step_times[k]);
+    }
     double* d_tiles = (double*)take(lb);
     int* d_err = (int*)(buf + off);
     std::vector<long long> flags(avg_flags, avg_flags + n_steps);
@@ -228,6 +237,7 @@ int hmc_exact_greeks_chunks(const hmc_model* model, const hmc_product* product, 
     if (ce == cudaSuccess) ce = cudaMemcpyAsync(d_f, flags.data(), fb, cudaMemcpyHostToDevice, st);
     if (ce == cudaSuccess) ce = cudaMemcpyAsync(d_k, keys.data(), kb, cudaMemcpyHostToDevice, st);
     if (ce == cudaSuccess && vb) ce = cudaMemcpyAsync(d_v, sim->sobol_v, vb, cudaMemcpyHostToDevice, st);
+    if (ce == cudaSuccess && eb) ce = cudaMemcpyAsync(d_e, em.data(), eb, cudaMemcpyHostToDevice, st);
     if (ce == cudaSuccess) ce = cudaMemsetAsync(d_err, 0, sizeof(int), st);
     for (long long r0 = 0; ce == cudaSuccess && r0 < R; r0 += batch) {
         const int nb = (int)std::min(batch, R - r0);
@@ -250,6 +260,7 @@ int hmc_exact_greeks_chunks(const hmc_model* model, const hmc_product* product, 
             e.sobol_scramble = sim->sobol_scramble ? 1 : 0;
             e.sobol_n_paths = sim->n_paths;
             e.out = d_obs[v];
+            e.rbump = v == 0 ? d_e : nullptr;
             e.scratch = d_s;
             e.err_flag = d_err;
             ce = hmc::launch_exact(e, grid, variant, st);

@@ -103,6 +103,11 @@ struct KernelArgs {
     float f_log2e;
     float f_rho, f_sq1mr2;
     float f_sqdt;    // sqrt(dt)
+    // Sobol drivers: the quantile's per-coordinate scales k (sqrt(2) folded in:
+    // .x -> z1l, .y -> sigma sqrt(dt) sqrt(1 - rho^2) z_b), -2k, and
+    // sigma rho / log2(e); host-computed in the float order the kernel used
+    float2 f_sob_k, f_sob_k2;
+    float f_sob_crho;
     // fp32 epilogue constants (no double->float conversions or divisions on
     // the device: F2F and MUFU.RCP share the MIO queue with the path MUFUs)
     float f_v0, f_vu, f_vd;

@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(kExactThreads, MINB) exact_batch_kernel(const 
         const unsigned long long key_path = derive(e.key_runs[run], (unsigned long long)(e.path_lo + p));
         const unsigned long long main_key = derive(key_path, 0ULL);
         const unsigned long long gamma_root = derive(key_path, 1ULL);
-        double ln_s = log(e.s0), v = e.v0, price_sum = 0.0, tw_sum = 0.0;
+        double ln_s = log(e.s0), v = e.v0, price_sum = 0.0, tw_sum = 0.0, dp_sum = 0.0, dm_sum = 0.0;
         const double* urow = e.uniforms ? e.uniforms + (size_t)i * 3 * e.n_steps : nullptr;
         // on-device Sobol (engine.py:97-101): point 1 + run N + path, or points
         // 1..N under per-(run, dimension) digital shifts (randomised QMC)
@@ -490,16 +490,26 @@ __global__ void __launch_bounds__(kExactThreads, MINB) exact_batch_kernel(const 
                 const double s_now = exp(ln_s);
                 price_sum += s_now;
                 tw_sum += s_now * e.times[k + 1];
+                if (e.rbump) {
+                    dp_sum += s_now * e.rbump[2 * (k + 1)];
+                    dm_sum += s_now * e.rbump[2 * (k + 1) + 1];
+                }
             }
         }
+        const int cols = e.rbump ? 5 : 3;
+        double* o = e.out + (size_t)i * cols;
         if (err != kErrNone) {
             atomicMax(e.err_flag, err);
-            e.out[3 * i] = e.out[3 * i + 1] = e.out[3 * i + 2] = 0.0;
+            for (int c = 0; c < cols; ++c) o[c] = 0.0;
             continue;
         }
-        e.out[3 * i + 0] = exp(ln_s);
-        e.out[3 * i + 1] = price_sum / e.n_dates;
-        e.out[3 * i + 2] = tw_sum / e.n_dates;
+        o[0] = exp(ln_s);
+        o[1] = price_sum / e.n_dates;
+        o[2] = tw_sum / e.n_dates;
+        if (e.rbump) {  // the r +- h_r averages are A + these (r enters only the drift)
+            o[3] = dp_sum / e.n_dates;
+            o[4] = dm_sum / e.n_dates;
+        }
     }
 }
 
@@ -508,28 +518,31 @@ __global__ void __launch_bounds__(kExactThreads, MINB) exact_batch_kernel(const 
 // simulations, reduced per 128-path tile like the discretised kernels --
 // so exact-scheme jobs use the same chunk exchange and fixed-shape run
 // reduction (bit-identical for any number of GPUs).
-//   obs*: [run][n][3] (s_T, avg, tw_sum); U/D: v0 +- bumps; P/M: r +- h_r
-//   (Asian only; European r bumps rescale S_T by e^{+-h T}).
+//   obs*: [run][n][3] (s_T, avg, tw_sum); U/D: v0 +- bumps.  The r +- h_r
+//   underlyings need no extra simulation: r enters the scheme only through
+//   the log-price drift (_core.pyx exact step), so S_k(r +- h) = S_k e^{+-h t_k}
+//   exactly -- European: S_T e^{+-h T}; Asian: A + (1/N) sum S_k expm1(+-h t_k),
+//   the base run's columns 3 and 4 ([run][n][5]), as the discretised kernels do.
 __global__ void __launch_bounds__(kTile) exact_estimator_kernel(const KernelArgs a, const double* __restrict__ o0,
                                                                 const double* __restrict__ oU,
-                                                                const double* __restrict__ oD,
-                                                                const double* __restrict__ oP,
-                                                                const double* __restrict__ oM, long long n,
+                                                                const double* __restrict__ oD, long long n,
                                                                 double ehT, double emhT, double* __restrict__ tiles,
                                                                 long long n_tiles, int run0) {
     const int run = blockIdx.y;
     const long long i = (long long)blockIdx.x * kTile + threadIdx.x;
     const bool live = i < n;
-    const size_t row = ((size_t)run * n + (live ? i : 0)) * 3;
+    const size_t idx = (size_t)run * n + (live ? i : 0);
+    const bool rcols = a.want_greeks && a.is_asian;
+    const size_t row = idx * (rcols ? 5 : 3);
     const int col = a.is_asian ? 1 : 0;
     const double A = o0[row + col], tw = o0[row + 2];
     double Au = A, Ad = A, Rp = A * ehT, Rm = A * emhT;
     if (a.want_greeks) {
-        Au = oU[row + col];
-        Ad = oD[row + col];
+        Au = oU[idx * 3 + col];
+        Ad = oD[idx * 3 + col];
         if (a.is_asian) {
-            Rp = oP[row + 1];
-            Rm = oM[row + 1];
+            Rp = A + o0[row + 3];
+            Rm = A + o0[row + 4];
         }
     }
     double q[kNQ];
@@ -541,12 +554,11 @@ __global__ void __launch_bounds__(kTile) exact_estimator_kernel(const KernelArgs
     tile_reduce_store(q, tiles + ((size_t)(run0 + run) * n_tiles + blockIdx.x) * kNW);
 }
 
-cudaError_t launch_exact_estimators(const KernelArgs& a, const double* const obs[5], long long n, int n_runs,
+cudaError_t launch_exact_estimators(const KernelArgs& a, const double* const obs[3], long long n, int n_runs,
                                     double ehT, double emhT, double* tiles, long long n_tiles, int run0,
                                     cudaStream_t s) {
     dim3 grid((unsigned)((n + kTile - 1) / kTile), (unsigned)n_runs);
-    exact_estimator_kernel<<<grid, kTile, 0, s>>>(a, obs[0], obs[1], obs[2], obs[3], obs[4], n, ehT, emhT, tiles,
-                                                  n_tiles, run0);
+    exact_estimator_kernel<<<grid, kTile, 0, s>>>(a, obs[0], obs[1], obs[2], n, ehT, emhT, tiles, n_tiles, run0);
     return cudaGetLastError();
 }
 

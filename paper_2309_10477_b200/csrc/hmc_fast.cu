@@ -76,8 +76,7 @@ __device__ __forceinline__ void sobol_paths(PathState32& st, int run, long long 
     //   .x = sqrt(dt) log2(e) z_a                        (= z1l)
     //   .y = sigma sqrt(dt) sqrt(1 - rho^2) z_b
     // and sz2 = sigma sqrt(dt) (rho z_a + sqrt(1 - rho^2) z_b) = .y + z1l sigma rho / log2(e)
-    const float2 k = make_float2(kSqrt2f * a.f_sqdt * a.f_log2e, kSqrt2f * a.f_sigma * a.f_sqdt * a.f_sq1mr2);
-    const float crho = a.f_sigma * a.f_rho / a.f_log2e;
+    // (host-computed: a.f_sob_k, a.f_sob_k2 = -2k, a.f_sob_crho = sigma rho / log2(e))
 
 #pragma unroll 1
     for (int k0 = 1; k0 <= a.n_sim; k0 += kSobolSteps) {
@@ -85,14 +84,17 @@ __device__ __forceinline__ void sobol_paths(PathState32& st, int run, long long 
         sobol_refill(tab, k0 - 1, m, sl, a);
         // the next step's table coordinates are loaded one step ahead (the
         // XOR consuming the LDS was the top stall site; 3.33 -> 3.29 ms;
-        // two steps ahead: 3.45)
+        // two steps ahead: 3.45) -- unconditionally, into the tables' pad
+        // step at the end of a chunk; the fixing weights through a chunk
+        // pointer, so the unrolled loads take immediate offsets
+        const float4* __restrict__ wk = per_thread_ptr(a.steps32 + k0);
         uint2 Xn = sobol_coords(tab, 0, sl);
         HMC_UNROLL(HMC_SOBOL_UNROLL)
         for (int q = 0; q < m; ++q) {
             const uint2 X = Xn;
-            if (q + 1 < m) Xn = sobol_coords(tab, q + 1, sl);
-            const float2 z = sobol_normal_X2(X.x, X.y, k);
-            step<FIX, GREEKS, true>(st, k0 + q, z.x, fmaf(z.x, crho, z.y), a);
+            Xn = sobol_coords(tab, q + 1, sl);
+            const float2 z = sobol_normal_X2(X.x, X.y, a.f_sob_k, a.f_sob_k2);
+            step_w<FIX, GREEKS, true>(st, wk + q, z.x, fmaf(z.x, a.f_sob_crho, z.y), a);
         }
     }
 }
@@ -184,11 +186,7 @@ __global__ void HMC_BOUNDS fast_greeks_kernel(const KernelArgs a,
     const long long p = live ? path : a.path_lo;
 
     PathState32 st;
-    st.v0 = a.f_v0;
-    st.vb = make_float2(a.f_vu, a.f_vd);
-    st.L0 = st.A0 = 0.0f;
-    st.Lb = st.Ab = make_float2(0.0f, 0.0f);
-    st.T1 = st.Dp = st.Dm = 0.0f;
+    st.init(a.f_v0, make_float2(a.f_vu, a.f_vd));
 
     if (SAMPLER == HMC_SAMPLER_PSEUDO) {
         // counter (step triple, path, key_run lo, key_run hi), fixed key;
@@ -229,11 +227,11 @@ __global__ void HMC_BOUNDS fast_greeks_kernel(const KernelArgs a,
     if (FIX == kFixLast) fixing<GREEKS>(st, __ldg(a.steps32 + a.n_sim));
 
     const float inv_n = a.f_inv_navg;
-    const float A = st.A0 * inv_n;
+    const float A = st.AT.x * inv_n;
     double q[kNQ];
     if (GREEKS) {
-        greeks_epilogue_f32(a, A, st.T1 * inv_n, st.Ab.x * inv_n, st.Ab.y * inv_n, st.Dp * inv_n,
-                            st.Dm * inv_n, q);
+        greeks_epilogue_f32(a, A, st.AT.y * inv_n, st.Ab.x * inv_n, st.Ab.y * inv_n, st.D.x * inv_n,
+                            st.D.y * inv_n, q);
     } else {
         const float K = a.f_K, disc = a.f_disc;
         q[0] = (double)(a.is_call ? disc * pos_part(A - K) : disc * pos_part(K - A));
@@ -281,11 +279,7 @@ __global__ void __launch_bounds__(kTile) given_normals_kernel(const KernelArgs a
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     PathState32 st;
-    st.v0 = a.f_v0;
-    st.vb = make_float2(a.f_vu, a.f_vd);
-    st.L0 = st.A0 = 0.0f;
-    st.Lb = st.Ab = make_float2(0.0f, 0.0f);
-    st.T1 = st.Dp = st.Dm = 0.0f;
+    st.init(a.f_v0, make_float2(a.f_vu, a.f_vd));
     const float c1 = a.f_sqdt * a.f_log2e, cs = a.f_sigma * a.f_sqdt;
     for (int k = 1; k <= a.n_sim; ++k) {
         const float2 w = z[(size_t)i * a.n_sim + (k - 1)];
@@ -293,9 +287,9 @@ __global__ void __launch_bounds__(kTile) given_normals_kernel(const KernelArgs a
     }
     if (FIX == kFixLast) fixing<true>(st, __ldg(a.steps32 + a.n_sim));
     const float inv_n = a.f_inv_navg;
-    const float A = st.A0 * inv_n;
+    const float A = st.AT.x * inv_n;
     double q[kNQ];
-    greeks_epilogue_f32(a, A, st.T1 * inv_n, st.Ab.x * inv_n, st.Ab.y * inv_n, st.Dp * inv_n, st.Dm * inv_n,
+    greeks_epilogue_f32(a, A, st.AT.y * inv_n, st.Ab.x * inv_n, st.Ab.y * inv_n, st.D.x * inv_n, st.D.y * inv_n,
                         q);
 #pragma unroll
     for (int j = 0; j < kNQ; ++j) out[(size_t)i * kNQ + j] = q[j];

@@ -83,7 +83,9 @@ struct ExactArgs {
     const uint32_t* sobol_v; // [30][3 n_steps] Sobol direction numbers (device) or null
     int sobol_scramble;      // digital shifts per (run, dimension)
     long long sobol_n_paths; // N of the run blocks 1 + run N + path
-    double* out;             // [n_runs][n][3]
+    double* out;             // [n_runs][n][3], or [n_runs][n][5] with rbump
+    const double* rbump;     // [n_steps + 1][2] expm1(+-h_r t_k), or null: the r +- h_r
+                             // averages as extra columns (see exact_batch_kernel)
     double* scratch;         // [kExactCacheNodes][grid threads]
     int* err_flag;           // max reference error code seen
 };
@@ -93,7 +95,7 @@ struct ExactArgs {
 cudaError_t exact_plan(long long rows, int sms, int* grid, int* variant);
 cudaError_t launch_exact(const ExactArgs& e, int grid, int variant, cudaStream_t s);
 // per-path exact-scheme estimators -> tiles[run0 + run][tile][HMC_NW]
-cudaError_t launch_exact_estimators(const KernelArgs& a, const double* const obs[5], long long n, int n_runs,
+cudaError_t launch_exact_estimators(const KernelArgs& a, const double* const obs[3], long long n, int n_runs,
                                     double ehT, double emhT, double* tiles, long long n_tiles, int run0,
                                     cudaStream_t s);
 

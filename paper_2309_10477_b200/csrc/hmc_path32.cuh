@@ -28,6 +28,16 @@ __device__ __forceinline__ float sqrta(float x) {
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// p, opaque to the compiler's uniformity analysis: a block-uniform table
+// pointer then stays in vector registers and unrolled loads through it take
+// immediate offsets (a uniform one costs a uniform-datapath address
+// computation plus two MOVs per load)
+template <class T>
+__device__ __forceinline__ const T* per_thread_ptr(const T* p) {
+    asm("mov.b64 %0, %0;" : "+l"(p));
+    return p;
+}
+
 // a float2 with both halves x (scalar operand of the paired FFMA2/FMUL2)
 __device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
 
@@ -185,7 +195,8 @@ __device__ __forceinline__ SobolTail sobol_tail2(float2 wc, float2 tf, uint32_t 
 // both coordinates of a step at once: the same per-lane arithmetic as the
 // scalar form (bit-identical), the float work as paired FFMA2/FMUL2; k is
 // the per-coordinate scale
-__device__ __forceinline__ float2 sobol_normal_X2(uint32_t Xa, uint32_t Xb, float2 k) {
+// k2 = -2k (callers in hot loops pass it precomputed)
+__device__ __forceinline__ float2 sobol_normal_X2(uint32_t Xa, uint32_t Xb, float2 k, float2 k2) {
     const float2 tf = make_float2(sobol_tail_frac(Xa), sobol_tail_frac(Xb));
     const float2 pr = __ffma2_rn(make_float2(-tf.x, -tf.y), tf, tf);
     const float2 wc = __ffma2_rn(make_float2(lg2a(pr.x), lg2a(pr.y)), f2(-kLn2), f2(-2.0f * kLn2 - 2.5f));
@@ -198,13 +209,17 @@ __device__ __forceinline__ float2 sobol_normal_X2(uint32_t Xa, uint32_t Xb, floa
     p = __ffma2_rn(p, wc, f2(-0.00417768164f));
     p = __ffma2_rn(p, wc, f2(0.246640727f));
     p = __ffma2_rn(p, wc, f2(1.50140941f));
-    if (__any_sync(0xffffffffu, fmaxf(wc.x, wc.y) >= 2.5f)) {
+    if (__builtin_expect(__any_sync(0xffffffffu, fmaxf(wc.x, wc.y) >= 2.5f), 0)) {
         const SobolTail r = sobol_tail2(wc, tf, Xa, Xb, k, p);
         if (r.done) return r.v;
         p = r.v;
     }
-    const float2 xk = __ffma2_rn(tf, make_float2(-2.0f * k.x, -2.0f * k.y), k);   // k |2u - 1|
+    const float2 xk = __ffma2_rn(tf, k2, k);   // k |2u - 1|
     return __fmul2_rn(p, make_float2(sobol_sign(xk.x, Xa), sobol_sign(xk.y, Xb)));
+}
+
+__device__ __forceinline__ float2 sobol_normal_X2(uint32_t Xa, uint32_t Xb, float2 k) {
+    return sobol_normal_X2(Xa, Xb, k, make_float2(-2.0f * k.x, -2.0f * k.y));
 }
 
 constexpr float kSqrt2f = 1.41421356237309504880f;
@@ -214,9 +229,17 @@ constexpr float kSqrt2f = 1.41421356237309504880f;
 // v0 - h floored at 0) so their updates issue as sm_100 paired FFMA2 --
 // the same IEEE fma per lane, half the issue slots.
 struct PathState32 {
-    float v0, L0, A0;      // base trajectory
+    float v0, L0;          // base trajectory
+    float2 AT;             // base: (fixing sum A0, sum S t)
+    float2 D;              // base: (sum S expm1(h t), sum S expm1(-h t))
     float2 vb, Lb, Ab;     // bumped pair
-    float T1, Dp, Dm;      // base: sum S t, sum S expm1(h t), sum S expm1(-h t)
+
+    __device__ __forceinline__ void init(float v0_, float2 vb_) {
+        v0 = v0_;
+        vb = vb_;
+        L0 = 0.0f;
+        AT = D = Lb = Ab = make_float2(0.0f, 0.0f);
+    }
 };
 
 __device__ __forceinline__ void traj_step(float& v, float& L, float z1l, float sz2, float ck,
@@ -256,11 +279,18 @@ __device__ __forceinline__ void advance(PathState32& st, float z1l, float sz2, c
 template <bool GREEKS, bool PAIR = false>
 __device__ __forceinline__ void fixing(PathState32& st, const float4 w) {
     const float P = ex2a(st.L0);
-    st.A0 = fmaf(P, w.x, st.A0);
+    if (!GREEKS) {
+        st.AT.x = fmaf(P, w.x, st.AT.x);
+    } else if (PAIR) {   // the same four fmas as paired FFMA2 (issue-bound drivers)
+        st.AT = __ffma2_rn(f2(P), make_float2(w.x, w.y), st.AT);
+        st.D = __ffma2_rn(f2(P), make_float2(w.z, w.w), st.D);
+    } else {
+        st.AT.x = fmaf(P, w.x, st.AT.x);
+        st.AT.y = fmaf(P, w.y, st.AT.y);
+        st.D.x = fmaf(P, w.z, st.D.x);
+        st.D.y = fmaf(P, w.w, st.D.y);
+    }
     if (GREEKS) {
-        st.T1 = fmaf(P, w.y, st.T1);
-        st.Dp = fmaf(P, w.z, st.Dp);
-        st.Dm = fmaf(P, w.w, st.Dm);
         // (carrying Au - A0 instead -- one more FADD per trajectory and
         // fixing -- shrinks Vega's fp32 error ~40x but costs 4 % of the
         // daily-fixing kernel: 10.66 -> 11.08 ms; not taken)
@@ -273,17 +303,24 @@ __device__ __forceinline__ void fixing(PathState32& st, const float4 w) {
     }
 }
 
-// PAIR: the bumped trajectories as paired FFMA2 (see traj_step2)
+// PAIR: the bumped trajectories as paired FFMA2 (see traj_step2); wk: this
+// step's fixing-weight entry (a.steps32 + k)
+template <int FIX, bool GREEKS, bool PAIR = false>
+__device__ __forceinline__ void step_w(PathState32& st, const float4* wk, float z1l, float sz2,
+                                       const KernelArgs& a) {
+    advance<GREEKS, PAIR>(st, z1l, sz2, a);
+    if (FIX == kFixEvery) {
+        fixing<GREEKS, PAIR>(st, __ldg(wk));
+    } else if (FIX == kFixTable) {
+        const float4 w = __ldg(wk);
+        if (w.x != 0.0f) fixing<GREEKS, PAIR>(st, w);
+    }
+}
+
 template <int FIX, bool GREEKS, bool PAIR = false>
 __device__ __forceinline__ void step(PathState32& st, int k, float z1l, float sz2,
                                      const KernelArgs& a) {
-    advance<GREEKS, PAIR>(st, z1l, sz2, a);
-    if (FIX == kFixEvery) {
-        fixing<GREEKS, PAIR>(st, __ldg(a.steps32 + k));
-    } else if (FIX == kFixTable) {
-        const float4 w = __ldg(a.steps32 + k);
-        if (w.x != 0.0f) fixing<GREEKS, PAIR>(st, w);
-    }
+    step_w<FIX, GREEKS, PAIR>(st, a.steps32 + k, z1l, sz2, a);
 }
 
 }  // namespace hmc

@@ -28,12 +28,15 @@ namespace hmc {
 #endif
 constexpr int kSobolSteps = HMC_SOBOL_STEPS;  // steps per table refill (2 dimensions each, <= 64)
 
+// One pad step per row: a driver may load pair q + 1 = STEPS unconditionally
+// (its one-ahead prefetch at the end of a chunk; the value is never used),
+// which keeps the unrolled step loop free of predicates and register copies.
 template <int STEPS, int WARPS>
 struct SobolTablesT {
     static constexpr int kSteps = STEPS;
     static constexpr int kRows = WARPS + 1;
-    uint2 T[STEPS][32];      // lane parts, (dim 2q, dim 2q+1)
-    uint2 U[kRows][STEPS];   // high parts of the block's aligned 32-point blocks
+    uint2 T[STEPS + 1][32];      // lane parts, (dim 2q, dim 2q+1)
+    uint2 U[kRows][STEPS + 1];   // high parts of the block's aligned 32-point blocks
 };
 
 // Gray-code split of this thread's point index (see above)
@@ -105,7 +108,7 @@ __device__ __forceinline__ void sobol_refill(Tab& tab, int q0, int m, const Sobo
                     u ^= __ldg(V + (__ffs(bits) - 1) * dim + d);
                 g = g2;
             }
-            out[r * 2 * Tab::kSteps] = ((u ^ sh) << 2) | sl.mid;   // left-aligned, midpoint bit
+            out[r * 2 * (Tab::kSteps + 1)] = ((u ^ sh) << 2) | sl.mid;   // left-aligned, midpoint bit
         }
     }
     __syncthreads();

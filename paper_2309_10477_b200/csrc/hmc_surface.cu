@@ -137,10 +137,10 @@ __device__ __forceinline__ void surface_checkpoint(const PathState32& st, const 
         // Asian: average of S over grid dates t_1..t_m;
         // a = [A (d+ - d-) + (d+ D+ - d- D-)/N] / 2h_r, both terms same sign
         const float inv = mc.inv_n;
-        const float Aa = st.A0 * inv;
-        const float al = (Aa * mc.ddisc + (mc.dp * st.Dp - mc.dm * st.Dm) * inv) * s.inv_2hr;
+        const float Aa = st.AT.x * inv;
+        const float al = (Aa * mc.ddisc + (mc.dp * st.D.x - mc.dm * st.D.y) * inv) * s.inv_2hr;
         surface_update(hist + per_style, g_asian, nb, sK, pow2, s.nK, s, mc.d, Aa, st.Ab.x * inv, st.Ab.y * inv,
-                       fmaf(st.Dp, inv, Aa), fmaf(st.Dm, inv, Aa), fmaf(st.T1, inv, -mc.T * Aa), al);
+                       fmaf(st.D.x, inv, Aa), fmaf(st.D.y, inv, Aa), fmaf(st.AT.y, inv, -mc.T * Aa), al);
     }
     __syncthreads();
     // flush this maturity's block histograms into the run accumulators
@@ -185,11 +185,7 @@ __global__ void __launch_bounds__(kSurfThreads, kSurfMinBlocks) surface_kernel(c
         const bool live = path < a.path_hi;
         const uint32_t c1 = (uint32_t)(live ? path : a.path_lo);
         PathState32 st;
-        st.v0 = a.f_v0;
-        st.vb = make_float2(a.f_vu, a.f_vd);
-        st.L0 = st.A0 = 0.0f;
-        st.Lb = st.Ab = make_float2(0.0f, 0.0f);
-        st.T1 = st.Dp = st.Dm = 0.0f;
+        st.init(a.f_v0, make_float2(a.f_vu, a.f_vd));
         int m = 0, next = s.mats[0].step;
         if (SAMPLER == HMC_SAMPLER_SOBOL) {
             // the single-product Sobol driver's points and quantile (same

@@ -25,6 +25,8 @@ VARIANT_SETS = {
     # bridge-ordered Sobol (time with HMC_VARIANT_SOBOL=1 HMC_VARIANT_BRIDGE=16)
     "bridge": {"b1": {}, "b2": {"HMC_BRIDGE_UNROLL": 2}, "b4": {"HMC_BRIDGE_UNROLL": 4},
                "b8": {"HMC_BRIDGE_UNROLL": 8}},
+    # A/B of two prebuilt libraries dropped into _variants/ as libhmc_a.so / libhmc_b.so
+    "ab": {"a": None, "b": None},
 }
 VARIANTS = VARIANT_SETS[os.environ.get("HMC_VARIANT_SET", "occupancy")]
 
