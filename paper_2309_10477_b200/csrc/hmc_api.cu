@@ -495,10 +495,13 @@ int hmc_greeks_chunks(const hmc_model* model, const hmc_product* product, const 
     cudaStream_t s = (cudaStream_t)stream;
     char* w = (char*)d_work;
     double* d_tiles = (double*)w;
-    HMC_CK(cudaMemcpyAsync(w + P.off_st64, P.st64.data(), P.st64.size() * sizeof(StepD),
-                           cudaMemcpyHostToDevice, s));
-    HMC_CK(cudaMemcpyAsync(w + P.off_st32, P.st32.data(), P.st32.size() * sizeof(float4),
-                           cudaMemcpyHostToDevice, s));
+    {   // both step tables in one host->device copy (they are adjacent in the workspace)
+        const size_t b64 = P.st64.size() * sizeof(StepD), b32 = P.st32.size() * sizeof(float4);
+        std::vector<char> img(P.off_st32 - P.off_st64 + b32);
+        std::memcpy(img.data(), P.st64.data(), b64);
+        std::memcpy(img.data() + (P.off_st32 - P.off_st64), P.st32.data(), b32);
+        HMC_CK(cudaMemcpyAsync(w + P.off_st64, img.data(), img.size(), cudaMemcpyHostToDevice, s));
+    }
     P.a.steps64 = (const StepD*)(w + P.off_st64);
     P.a.steps32 = (const float4*)(w + P.off_st32);
     if (sim->sampler == HMC_SAMPLER_SOBOL) {

@@ -154,16 +154,23 @@ __device__ __forceinline__ void sobol_bridge_paths(PathState32& st, int run, lon
             }
             const int run = min(kend - k, c0 + kQ - pc);
             const int q0 = pc - c0;
+            // as the time-ordered driver: per-step tables through per-thread
+            // pointers (immediate offsets), coordinates loaded one step ahead
+            // (unconditionally: pair q0 + run <= kQ is the tables' pad step)
+            const BridgeStep* __restrict__ bsp = per_thread_ptr(a.bridge_steps32 + k);
+            const float4* __restrict__ wk = per_thread_ptr(a.steps32 + k);
+            uint2 Xn = sobol_coords(tab, q0, sl);
             HMC_UNROLL(HMC_BRIDGE_UNROLL)
             for (int i = 0; i < run; ++i) {
-                const BridgeStep bs = a.bridge_steps32[k + i];
-                float za, zb;
-                sobol_pair(tab, q0 + i, sl, za, zb);
-                const float d1 = fmaf(R.x - W1, bs.alpha, bs.beta * za);
-                const float d2 = fmaf(R.y - W2, bs.alpha, bs.beta * zb);
+                const BridgeStep bs = bsp[i];
+                const uint2 X = Xn;
+                Xn = sobol_coords(tab, q0 + i + 1, sl);
+                const float2 z = sobol_normal_X2(X.x, X.y, f2(1.0f));
+                const float d1 = fmaf(R.x - W1, bs.alpha, bs.beta * z.x);
+                const float d2 = fmaf(R.y - W2, bs.alpha, bs.beta * z.y);
                 W1 += d1;
                 W2 += d2;
-                step<FIX, GREEKS, true>(st, k + i, l2e * d1, sg * fmaf(rho, d1, sq1mr2 * d2), a);
+                step_w<FIX, GREEKS, true>(st, wk + i, l2e * d1, sg * fmaf(rho, d1, sq1mr2 * d2), a);
             }
             k += run;
             pc += run;

@@ -163,6 +163,18 @@ def summarise(config: SimConfig, sums: np.ndarray, wall_ms: float,
     ``sums`` is [n_runs, HMC_NW] = {sum, sum of squares} per quantity."""
     N, R = config.n_paths, config.n_runs
     M = R * N
+    if R == 1 and N > 1:
+        # one run: the same values without the numpy reductions on 1-element
+        # rows (np.mean of one value is that value; the run-level SD is 0)
+        row = sums[0].tolist()
+        out = {}
+        for q, name in enumerate(names):
+            s, ss = row[2 * q], row[2 * q + 1]
+            v = s / N
+            var = max(ss - s * s / M, 0.0) / (M - 1)
+            out[name] = McSummary(estimate=v, std_error=0.0, per_run_values=[v], wall_ms=wall_ms,
+                                  n_paths=N, n_runs=1, path_std_error=math.sqrt(var / M))
+        return out
     # one row per quantity, contiguous: the row reductions are exactly the
     # reference's 1-D np.mean / np.std per quantity (engine.py:133-135)
     runs = np.ascontiguousarray(sums[:, 0::2].T) / N
