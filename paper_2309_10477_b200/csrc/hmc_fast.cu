@@ -33,12 +33,15 @@
 // daily-fixing Asian is MUFU-queue bound and prefers 7 blocks (28 warps,
 // 72 regs: 48 warps 11.1 ms -> 28 warps 10.7 ms); the European (one ex2 at
 // the end) prefers 10 blocks (8.55 -> 8.40 ms).
+// The time-ordered Sobol Asian kernel runs 8 blocks (60 registers, no spills):
+// RQMC Asian 2^22 x 252 3.28 -> 3.18 ms against 7 blocks (6: 3.28).
 // The Brownian-bridge Sobol kernel keeps its skeleton in shared memory
 // (10 KB tables + (S + 1) KB skeleton per block), 7 blocks at S = 16.
 #ifdef HMC_MIN_BLOCKS
 #define HMC_BOUNDS __launch_bounds__(kTile, HMC_MIN_BLOCKS)
 #else
-#define HMC_BOUNDS __launch_bounds__(kTile, (SAMPLER == kSamplerBridge ? 7 : (FIX == kFixLast ? 10 : 7)))
+#define HMC_BOUNDS \
+    __launch_bounds__(kTile, (SAMPLER == kSamplerBridge ? 7 : (FIX == kFixLast ? 10 : SAMPLER == HMC_SAMPLER_SOBOL ? 8 : 7)))
 #endif
 
 namespace hmc {

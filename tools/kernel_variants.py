@@ -21,10 +21,13 @@ VDIR = os.path.join(ROOT, "paper_2309_10477_b200", "_variants")
 VARIANT_SETS = {
     "occupancy": {"base": {}, "lb6": {"HMC_MIN_BLOCKS": 6}, "lb8": {"HMC_MIN_BLOCKS": 8}},
     # RQMC Sobol driver (time with HMC_VARIANT_SOBOL=1)
-    "sobol": {"u8": {}, "u4": {"HMC_SOBOL_UNROLL": 4}},
+    "sobol": {"u8": {}, "u4": {"HMC_SOBOL_UNROLL": 4}, "u16": {"HMC_SOBOL_UNROLL": 16},
+              "u8lb8": {"HMC_MIN_BLOCKS": 8}, "u8lb6": {"HMC_MIN_BLOCKS": 6}},
     # bridge-ordered Sobol (time with HMC_VARIANT_SOBOL=1 HMC_VARIANT_BRIDGE=16)
     "bridge": {"b1": {}, "b2": {"HMC_BRIDGE_UNROLL": 2}, "b4": {"HMC_BRIDGE_UNROLL": 4},
                "b8": {"HMC_BRIDGE_UNROLL": 8}},
+    # European (time with HMC_VARIANT_EURO=1): resident blocks per SM
+    "euro": {"e10": {}, "e8": {"HMC_MIN_BLOCKS": 8}, "e12": {"HMC_MIN_BLOCKS": 12}, "e14": {"HMC_MIN_BLOCKS": 14}},
     # A/B of two prebuilt libraries dropped into _variants/ as libhmc_a.so / libhmc_b.so
     "ab": {"a": None, "b": None},
 }
