@@ -117,7 +117,21 @@ __device__ __forceinline__ void sobol_bridge_paths(PathState32& st, int run, lon
     float2* my = skel + threadIdx.x;  // point j at my[j * kTile]
     const SobolLane sl(run, p, a.path_lo + (long long)blockIdx.x * kTile, kWarps, a);
     const int S = a.bridge_segments;
-    const float l2e = a.f_log2e, sg = a.f_sigma;
+    // The bridge runs on the step-shock channels directly: every bridge
+    // formula is linear, so instead of (W1, W2) it carries
+    //   B = (log2(e) W1, sigma (rho W1 + sqrt(1 - rho^2) W2))
+    // whose increments ARE the step shocks (z1l, sz2) of step(): the
+    // quantile takes the scales k = (log2 e, sigma sqrt(1 - rho^2)) and
+    // z'.y += (sigma rho / log2 e) z'.x correlates them.  Per fine step that
+    // is one FADD2 + FMUL2 + FFMA2 + FADD2 instead of ~12 scalar instructions.
+    const float2 kq = make_float2(a.f_log2e, a.f_sigma * a.f_sq1mr2);
+    const float crho = a.f_sob_crho;
+    auto shocks = [&](int q) {
+        const uint2 X = sobol_coords(tab, q, sl);
+        float2 z = sobol_normal_X2(X.x, X.y, kq);
+        z.y = fmaf(z.x, crho, z.y);
+        return z;
+    };
 
     int c0 = 0;  // first pair of the loaded chunk
     sobol_refill(tab, 0, min(kQ, a.n_sim), sl, a);
@@ -128,23 +142,20 @@ __device__ __forceinline__ void sobol_bridge_paths(PathState32& st, int run, lon
             c0 = i;
             sobol_refill(tab, c0, min(kQ, a.n_sim - c0), sl, a);
         }
-        float za, zb;
-        sobol_pair(tab, i - c0, sl, za, zb);
+        const float2 z = shocks(i - c0);
         const BridgeNode nd = a.bridge_nodes32[i];
         const float2 wl = my[(nd.lr & 0xffff) * kTile], wr = my[(nd.lr >> 16) * kTile];
-        my[nd.m * kTile] = make_float2(fmaf(nd.sd, za, fmaf(nd.a, wr.x - wl.x, wl.x)),
-                                       fmaf(nd.sd, zb, fmaf(nd.a, wr.y - wl.y, wl.y)));
+        my[nd.m * kTile] = __ffma2_rn(f2(nd.sd), z, __ffma2_rn(f2(nd.a), sub2(wr, wl), wl));
     }
     // time order, segment by segment: segment j covers steps b_{j-1}+1 .. b_j,
     // b_j = j n_sim / S (the host's build_bridge); its fine steps draw the
     // next pairs and move towards the skeleton point R, the last step lands
-    // on it (alpha = 1, beta = 0: d = R - W).  The fine steps run as a
+    // on it (alpha = 1, beta = 0: d = R - B).  The fine steps run as a
     // regular loop between table refills, unrolled so the quantiles of
     // later steps overlap the trajectory updates of earlier ones.
     int pc = S;  // next pair
-    float W1 = 0.0f, W2 = 0.0f;
+    float2 B = make_float2(0.0f, 0.0f);
     int k = 1;
-    const float rho = a.f_rho, sq1mr2 = a.f_sq1mr2;
 #pragma unroll 1
     for (int j = 1; j <= S; ++j) {
         const float2 R = my[j * kTile];
@@ -158,30 +169,23 @@ __device__ __forceinline__ void sobol_bridge_paths(PathState32& st, int run, lon
             const int run = min(kend - k, c0 + kQ - pc);
             const int q0 = pc - c0;
             // as the time-ordered driver: per-step tables through per-thread
-            // pointers (immediate offsets), coordinates loaded one step ahead
-            // (unconditionally: pair q0 + run <= kQ is the tables' pad step)
+            // pointers (immediate offsets)
             const BridgeStep* __restrict__ bsp = per_thread_ptr(a.bridge_steps32 + k);
             const float4* __restrict__ wk = per_thread_ptr(a.steps32 + k);
-            uint2 Xn = sobol_coords(tab, q0, sl);
             HMC_UNROLL(HMC_BRIDGE_UNROLL)
             for (int i = 0; i < run; ++i) {
                 const BridgeStep bs = bsp[i];
-                const uint2 X = Xn;
-                Xn = sobol_coords(tab, q0 + i + 1, sl);
-                const float2 z = sobol_normal_X2(X.x, X.y, f2(1.0f));
-                const float d1 = fmaf(R.x - W1, bs.alpha, bs.beta * z.x);
-                const float d2 = fmaf(R.y - W2, bs.alpha, bs.beta * z.y);
-                W1 += d1;
-                W2 += d2;
-                step_w<FIX, GREEKS, true>(st, wk + i, l2e * d1, sg * fmaf(rho, d1, sq1mr2 * d2), a);
+                const float2 z = shocks(q0 + i);
+                const float2 d = __ffma2_rn(sub2(R, B), f2(bs.alpha), __fmul2_rn(f2(bs.beta), z));
+                B = __fadd2_rn(B, d);
+                step_w<FIX, GREEKS, true>(st, wk + i, d.x, d.y, a);
             }
             k += run;
             pc += run;
         }
-        const float d1 = R.x - W1, d2 = R.y - W2;    // segment end
-        W1 = R.x;
-        W2 = R.y;
-        step<FIX, GREEKS, true>(st, k, l2e * d1, sg * fmaf(rho, d1, sq1mr2 * d2), a);
+        const float2 d = sub2(R, B);    // segment end
+        B = R;
+        step<FIX, GREEKS, true>(st, k, d.x, d.y, a);
         ++k;
     }
 }

@@ -40,6 +40,8 @@ __device__ __forceinline__ const T* per_thread_ptr(const T* p) {
 
 // a float2 with both halves x (scalar operand of the paired FFMA2/FMUL2)
 __device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
+// paired a - b (one FFMA2 with b * -1: exact product, one rounding, = a - b)
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __ffma2_rn(b, f2(-1.0f), a); }
 
 // uniform in [1, 2) from the top 23 bits of x: one LEA.HI
 __device__ __forceinline__ float one_to_two(uint32_t x) {
