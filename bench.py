@@ -471,7 +471,10 @@ def run_b200(args) -> None:
             "estimates": {q: [g[q].estimate, g[q].path_std_error] for q in g} if g else None,
         }
         if distributed:
-            line["dist_backend"] = "gloo (host-staged)" if gloo else "nccl (libhmc communicator)"
+            why = parallel.comm_fallback_reason()
+            line["dist_backend"] = ("gloo (host-staged)" if gloo else
+                                    "nccl (libhmc communicator)" if why is None else
+                                    f"nccl (torch process group; libhmc communicator unavailable: {why})")
         if world == 1 and not args.no_cpu:
             line["cpu_baseline"] = cpu_baseline_block()
         if secondary is not None:

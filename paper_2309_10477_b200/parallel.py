@@ -147,6 +147,37 @@ def close_comms() -> None:
 # ---------------------------------------------------------------------------
 # the exchanges the engine uses
 # ---------------------------------------------------------------------------
+# (process group, device) pairs whose libhmc communicator could not be
+# created: their exchanges go through the group's own collectives (the same
+# bytes in the same order), reported once on stderr
+_COMM_FAILED: dict = {}
+
+
+def comm_fallback_reason(group=None, device_index=None):
+    """Why the libhmc communicator of (group, device) is not in use, or None."""
+    if device_index is None:
+        return next(iter(_COMM_FAILED.values()), None)
+    return _COMM_FAILED.get((id(group) if group is not None else None, device_index))
+
+
+def _libhmc_comm(group, device):
+    """The group's libhmc communicator, or None if it cannot be created (then
+    every rank of the group falls back to the group's collectives: a failure
+    to open or initialise NCCL is the same on every rank)."""
+    import sys
+    from .errors import HestonError
+    key = (id(group) if group is not None else None, device.index)
+    if key in _COMM_FAILED:
+        return None
+    try:
+        return comm_for(group, device)
+    except HestonError as e:
+        _COMM_FAILED[key] = str(e)
+        print(f"paper_2309_10477_b200.parallel: libhmc NCCL communicator unavailable ({e}); "
+              "exchanging chunk partials through the process group instead", file=sys.stderr)
+        return None
+
+
 def gather_chunks(local, n_paths: int, group=None):
     """All-gather per-rank chunk partials ``local[run, chunk, HMC_NW]`` into
     the global ``[run, C, HMC_NW]`` tensor in path order (same device/dtype
@@ -158,28 +189,38 @@ def gather_chunks(local, n_paths: int, group=None):
     n_runs = local.shape[0]
     C = n_chunks(n_paths)
     if _uses_nccl(group, local):
-        full = torch.empty((n_runs, C, HMC_NW), dtype=local.dtype, device=local.device)
-        stream = torch.cuda.current_stream(local.device)
-        comm_for(group, local.device).gather_chunks(local.contiguous(), n_runs, n_paths, full, stream)
-        return full
-    return _gather_chunks_host(local, n_paths, group)
+        comm = _libhmc_comm(group, local.device)
+        if comm is not None:
+            full = torch.empty((n_runs, C, HMC_NW), dtype=local.dtype, device=local.device)
+            stream = torch.cuda.current_stream(local.device)
+            comm.gather_chunks(local.contiguous(), n_runs, n_paths, full, stream)
+            return full
+        return _gather_chunks_group(local, n_paths, group, on_device=True)
+    return _gather_chunks_group(local, n_paths, group, on_device=False)
 
 
-def _gather_chunks_host(local, n_paths: int, group=None):
-    """The gloo transport: stage through host memory, all-gather padded
-    slices, drop the padding, concatenate in rank (= path) order."""
+def _gather_chunks_group(local, n_paths: int, group=None, on_device: bool = False):
+    """The process group's own all-gather of padded slices (gloo: staged
+    through host memory; NCCL without a libhmc communicator: on the device),
+    padding dropped, concatenated in rank (= path) order."""
     import torch
     import torch.distributed as dist
     rank, world = world_info(group)
     n_runs = local.shape[0]
     slices = [shard(n_paths, r, world) for r in range(world)]
     width = max(s.n_chunks for s in slices)
-    send = torch.zeros((n_runs, width, HMC_NW), dtype=local.dtype)
-    send[:, : local.shape[1]] = local.cpu()
+    dev = local.device if on_device else torch.device("cpu")
+    send = torch.zeros((n_runs, width, HMC_NW), dtype=local.dtype, device=dev)
+    send[:, : local.shape[1]] = local.to(dev)
     recv = [torch.empty_like(send) for _ in range(world)]
     dist.all_gather(recv, send, group=group)
     parts = [recv[r][:, : slices[r].n_chunks] for r in range(world)]
     return torch.cat(parts, dim=1).contiguous().to(local.device)
+
+
+def _gather_chunks_host(local, n_paths: int, group=None):
+    """The gloo transport (host-staged)."""
+    return _gather_chunks_group(local, n_paths, group, on_device=False)
 
 
 def allreduce_sum(buf, group=None) -> None:
@@ -191,7 +232,11 @@ def allreduce_sum(buf, group=None) -> None:
     if world == 1:
         return
     if _uses_nccl(group, buf):
-        comm_for(group, buf.device).allreduce_sum(buf, torch.cuda.current_stream(buf.device))
+        comm = _libhmc_comm(group, buf.device)
+        if comm is not None:
+            comm.allreduce_sum(buf, torch.cuda.current_stream(buf.device))
+        else:
+            dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
         return
     host = buf.cpu()
     dist.all_reduce(host, op=dist.ReduceOp.SUM, group=group)

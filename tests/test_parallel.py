@@ -123,3 +123,53 @@ def test_gather_matches_single_process(world, n):
     # and therefore the fixed-order reduction is bit-identical across world sizes
     np.testing.assert_array_equal(_seq_reduce(torch.tensor(got[world - 1][0])),
                                   _seq_reduce(torch.tensor(single)))
+
+
+def _fallback_worker(rank, world, port, n, q):
+    """NCCL-group code path with a libhmc communicator that cannot be
+    created: every rank falls back to the group's own collectives."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.distributed.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2309_10477_b200.errors import DeviceError
+
+        def no_comm(group, device):
+            raise DeviceError("cannot open libnccl.so.2 (simulated)")
+        parallel._uses_nccl = lambda group, tensor: True
+        parallel.comm_for = no_comm
+        s = parallel.shard(n, rank, world)
+        local = torch.arange(s.n_chunks * HMC_NW, dtype=torch.float64).reshape(1, s.n_chunks, HMC_NW)
+        local += 1000.0 * s.chunk_lo
+        full = parallel.gather_chunks(local, n)
+        full2 = parallel.gather_chunks(local, n)        # second call: no retry, same answer
+        acc = torch.arange(10, dtype=torch.int64) * (rank + 1)
+        parallel.allreduce_sum(acc)
+        q.put((rank, full.numpy(), full2.numpy(), acc.numpy(), parallel.comm_fallback_reason()))
+    finally:
+        torch.distributed.destroy_process_group()
+
+
+def test_exchange_falls_back_without_libhmc_communicator():
+    world, n = 2, 5 * HMC_CHUNK + 9
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fallback_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = {r: rest for r, *rest in (q.get(timeout=300) for _ in procs)}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = []
+    for r in range(world):
+        s = parallel.shard(n, r, world)
+        want.append(np.arange(s.n_chunks * HMC_NW, dtype=np.float64).reshape(1, s.n_chunks, HMC_NW)
+                    + 1000.0 * s.chunk_lo)
+    want = np.concatenate(want, axis=1)
+    for r in range(world):
+        full, full2, acc, why = got[r]
+        np.testing.assert_array_equal(full, want)
+        np.testing.assert_array_equal(full2, want)
+        np.testing.assert_array_equal(acc, np.arange(10) * 3)
+        assert "simulated" in why
