@@ -93,8 +93,16 @@ __global__ void __launch_bounds__(kTile) replay_batch_kernel(const KernelArgs a,
     out[3 * i + 2] = t.tw / a.n_avg;
 }
 
+// 8 resident blocks (64 registers, the rest spilled to L1-resident local
+// memory): the fp64 pipe needs the warps to hide its latency.  Full-Greeks
+// replay, Asian daily fixings, 2^20 x 252 (tools/kernel_variants.py set
+// "replay"): unbounded (168-255 registers, 3 blocks) 14.1-18.0 ms, 4 blocks
+// 12.4, 5 12.05, 6 12.02, 8 11.93 ms; results identical.
+#ifndef HMC_REPLAY_MINB
+#define HMC_REPLAY_MINB 8
+#endif
 template <bool GREEKS>
-__global__ void __launch_bounds__(kTile) replay_greeks_kernel(const KernelArgs a,
+__global__ void __launch_bounds__(kTile, HMC_REPLAY_MINB) replay_greeks_kernel(const KernelArgs a,
                                                               double* __restrict__ tiles,
                                                               long long n_tiles) {
     const int run = a.run0 + (int)blockIdx.y;

@@ -28,6 +28,9 @@ VARIANT_SETS = {
                "b8": {"HMC_BRIDGE_UNROLL": 8}},
     # European (time with HMC_VARIANT_EURO=1): resident blocks per SM
     "euro": {"e10": {}, "e8": {"HMC_MIN_BLOCKS": 8}, "e12": {"HMC_MIN_BLOCKS": 12}, "e14": {"HMC_MIN_BLOCKS": 14}},
+    # fp64 replay greeks (time with HMC_VARIANT_FP64=1): resident blocks per SM
+    "replay": {"r1": {}, "r4": {"HMC_REPLAY_MINB": 4}, "r5": {"HMC_REPLAY_MINB": 5},
+               "r6": {"HMC_REPLAY_MINB": 6}, "r8": {"HMC_REPLAY_MINB": 8}},
     # A/B of two prebuilt libraries dropped into _variants/ as libhmc_a.so / libhmc_b.so
     "ab": {"a": None, "b": None},
 }
@@ -55,6 +58,8 @@ import os as _os, dataclasses as _dc
 if _os.environ.get("HMC_VARIANT_EURO"):
     from paper_2309_10477_b200 import OptionSpec as _OS
     spec = _OS("european", "call", 100.0, 1.0, 100.0)
+if _os.environ.get("HMC_VARIANT_FP64"):
+    cfg = _dc.replace(cfg, precision="fp64", n_paths=2**20)
 if _os.environ.get("HMC_VARIANT_SOBOL"):
     cfg = _dc.replace(cfg, sampler="sobol", sobol_highdim_ack=True, sobol_scramble=True, n_paths=2**22,
                       sobol_bridge=int(_os.environ.get("HMC_VARIANT_BRIDGE", "0")))

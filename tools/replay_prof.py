@@ -1,0 +1,19 @@
+"""One fp64 replay full-Greeks call (the reference's stream and arithmetic,
+Asian daily fixings, BASELINE params) for timing / ncu:
+python tools/replay_prof.py [n_paths]."""
+import os, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch
+from paper_2309_10477_b200 import BENCH_PARAMS, HestonParams, OptionSpec, SimConfig, greeks, daily_fixings
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 2 ** 20
+p = HestonParams(**BENCH_PARAMS)
+spec = OptionSpec("asian_arithmetic", "call", 100.0, 1.0, 100.0, averaging_times=daily_fixings(1.0, 252))
+cfg = SimConfig(scheme="milstein", n_paths=n, n_steps=252, n_runs=1, seed=42, precision="fp64")
+g = greeks(p, spec, cfg)
+ts = []
+for _ in range(3):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(); g = greeks(p, spec, cfg); e1.record(); torch.cuda.synchronize()
+    ts.append(e0.elapsed_time(e1))
+print("replay", n, "paths: %.2f ms" % min(ts), g["price"].estimate)
