@@ -94,6 +94,17 @@ def build(verbose: bool = False, force: bool = False, defines: dict | None = Non
     return lib
 
 
+CHECKED_LIB = os.path.join(PKG, "_variants", "libhmc_checked.so")
+
+
+def build_checked(verbose: bool = False, force: bool = False) -> str:
+    """The bounds-checked build (device asserts on every data- or
+    table-dependent index, csrc/hmc_device.cuh HMC_DCHECK) -- the stand-in
+    for compute-sanitizer (tests/test_gpu_checked.py); never the product."""
+    return build(verbose=verbose, force=force, defines={"HMC_DEBUG_BOUNDS": 1}, lib=CHECKED_LIB,
+                 objdir=os.path.join(PKG, "_variants", "obj_checked"))
+
+
 if __name__ == "__main__":
     build(verbose="--verbose" in sys.argv, force="--force" in sys.argv)
     print(LIB)

@@ -12,6 +12,18 @@
 
 #include "../../include/hmc.h"
 
+// Device-side bounds checks of every data- or table-dependent index
+// (shared tables, histograms, skeletons, node caches, step tables, tile
+// writes), compiled in only for the checked build (HMC_DEBUG_BOUNDS=1,
+// paper_2309_10477_b200/_variants/libhmc_checked.so, tests/test_gpu_checked.py):
+// the stand-in for compute-sanitizer, which is closed on this GPU pool.
+#if defined(HMC_DEBUG_BOUNDS) && HMC_DEBUG_BOUNDS
+#include <cassert>
+#define HMC_DCHECK(cond) assert(cond)
+#else
+#define HMC_DCHECK(cond) ((void)0)
+#endif
+
 namespace hmc {
 
 constexpr int kTile = HMC_TILE;
@@ -218,6 +230,7 @@ __device__ __forceinline__ void tile_reduce_store(const double (&q)[kNQ], double
         for (int i = 0; i < kNW; ++i) red[warp][i] = w[i];
     }
     __syncthreads();
+    HMC_DCHECK(blockDim.x == kTile);
     if (threadIdx.x < kNW) {
         double s = red[0][threadIdx.x];
 #pragma unroll

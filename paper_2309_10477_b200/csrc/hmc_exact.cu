@@ -220,6 +220,7 @@ struct NodeCache {
     const PhiPath* P;
     double h;
     __device__ double re(int j, int* err) const {  // j 0-based
+        HMC_DCHECK(j >= 0);
         if (j < cap) return base[(size_t)j * stride];
         return phi_node(*P, (j + 1) * h, err).re;
     }
@@ -428,6 +429,7 @@ __global__ void __launch_bounds__(kExactThreads, MINB) exact_batch_kernel(const 
     for (long long i = slot; i < total; i += stride) {
         int err = kErrNone;
         const long long run = i / n, p = i - run * n;
+        HMC_DCHECK(run < e.n_runs && slot < stride);
         const unsigned long long key_path = derive(e.key_runs[run], (unsigned long long)(e.path_lo + p));
         const unsigned long long main_key = derive(key_path, 0ULL);
         const unsigned long long gamma_root = derive(key_path, 1ULL);

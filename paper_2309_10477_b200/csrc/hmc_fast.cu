@@ -90,6 +90,7 @@ __device__ __forceinline__ void sobol_paths(PathState32& st, int run, long long 
         // two steps ahead: 3.45) -- unconditionally, into the tables' pad
         // step at the end of a chunk; the fixing weights through a chunk
         // pointer, so the unrolled loads take immediate offsets
+        HMC_DCHECK(k0 + m - 1 <= a.n_sim);
         const float4* __restrict__ wk = per_thread_ptr(a.steps32 + k0);
         uint2 Xn = sobol_coords(tab, 0, sl);
         HMC_UNROLL(HMC_SOBOL_UNROLL)
@@ -144,6 +145,7 @@ __device__ __forceinline__ void sobol_bridge_paths(PathState32& st, int run, lon
         }
         const float2 z = shocks(i - c0);
         const BridgeNode nd = a.bridge_nodes32[i];
+        HMC_DCHECK(nd.m >= 1 && nd.m <= S && (nd.lr & 0xffff) <= S && (nd.lr >> 16) <= S);
         const float2 wl = my[(nd.lr & 0xffff) * kTile], wr = my[(nd.lr >> 16) * kTile];
         my[nd.m * kTile] = __ffma2_rn(f2(nd.sd), z, __ffma2_rn(f2(nd.a), sub2(wr, wl), wl));
     }
@@ -168,6 +170,7 @@ __device__ __forceinline__ void sobol_bridge_paths(PathState32& st, int run, lon
             }
             const int run = min(kend - k, c0 + kQ - pc);
             const int q0 = pc - c0;
+            HMC_DCHECK(run >= 1 && q0 >= 0 && q0 + run <= kQ && k + run - 1 <= a.n_sim);
             // as the time-ordered driver: per-step tables through per-thread
             // pointers (immediate offsets)
             const BridgeStep* __restrict__ bsp = per_thread_ptr(a.bridge_steps32 + k);
@@ -215,6 +218,7 @@ __global__ void HMC_BOUNDS fast_greeks_kernel(const KernelArgs a,
             const uint4 x = philox4x32_10((uint32_t)j, c1, c2, c3);
             float fr[3], fa[3];
             tri_unpack(x, fr, fa);
+            HMC_DCHECK(k + 2 <= a.n_sim);
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
                 float z1l, sz2;
@@ -256,6 +260,7 @@ __global__ void HMC_BOUNDS fast_greeks_kernel(const KernelArgs a,
 #pragma unroll
         for (int i = 0; i < kNQ; ++i) q[i] = 0.0;
     }
+    HMC_DCHECK((long long)blockIdx.x < n_tiles && run < a.n_runs);
     tile_reduce_store(q, tiles + ((size_t)run * n_tiles + blockIdx.x) * kNW);
 }
 

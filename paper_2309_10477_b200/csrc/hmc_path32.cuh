@@ -322,6 +322,7 @@ __device__ __forceinline__ void step_w(PathState32& st, const float4* wk, float 
 template <int FIX, bool GREEKS, bool PAIR = false>
 __device__ __forceinline__ void step(PathState32& st, int k, float z1l, float sz2,
                                      const KernelArgs& a) {
+    HMC_DCHECK(k >= 1 && k <= a.n_sim);
     step_w<FIX, GREEKS, PAIR>(st, a.steps32 + k, z1l, sz2, a);
 }
 

@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(kTile, HMC_REPLAY_MINB) replay_greeks_kernel(c
             ref_step(tu, z1, z2, a);
             ref_step(td, z1, z2, a);
         }
+        HMC_DCHECK(k >= 1 && k <= a.n_sim);
         const StepD st = a.steps64[k];
         if (st.fix != 0.0) {
             t0.ps += t0.s;
@@ -164,6 +165,8 @@ __global__ void __launch_bounds__(kTile, HMC_REPLAY_MINB) replay_greeks_kernel(c
             double u1, u2;
             dr.get(i + 1, u1, u2);  // dimension pair i
             const BridgeNodeD nd = a.bridge_nodes64[i];
+            HMC_DCHECK(nd.m >= 1 && nd.m <= a.bridge_segments && nd.l <= a.bridge_segments &&
+                       nd.r <= a.bridge_segments);
             W1s[nd.m] = W1s[nd.l] + nd.a * (W1s[nd.r] - W1s[nd.l]) + nd.sd * ndtri_ref(u1);
             W2s[nd.m] = W2s[nd.l] + nd.a * (W2s[nd.r] - W2s[nd.l]) + nd.sd * ndtri_ref(u2);
         }
@@ -172,6 +175,7 @@ __global__ void __launch_bounds__(kTile, HMC_REPLAY_MINB) replay_greeks_kernel(c
         const double isq = 1.0 / sqrt(a.dt);
         for (int k = 1; k <= a.n_sim; ++k) {
             const BridgeStepD bs = a.bridge_steps64[k];
+            HMC_DCHECK(bs.j >= 1 && bs.j <= a.bridge_segments);
             double za = 0.0, zb = 0.0;
             if (bs.consume) {
                 double u1, u2;
@@ -191,6 +195,7 @@ __global__ void __launch_bounds__(kTile, HMC_REPLAY_MINB) replay_greeks_kernel(c
     // obs[:, 0] == obs[:, 1] (engine.py:51)
     const double A = t0.ps / a.n_avg;
     double q[kNQ];
+    HMC_DCHECK((long long)blockIdx.x < n_tiles);
     greeks_epilogue<double>(a, A, t0.tw / a.n_avg, tu.ps / a.n_avg, td.ps / a.n_avg,
                             A + dp / a.n_avg, A + dm / a.n_avg, q);
     if (!live) {

@@ -71,6 +71,7 @@ __device__ __forceinline__ void sobol_refill(Tab& tab, int q0, int m, const Sobo
     const int dim = a.sobol_dim;
     const int d0 = 2 * q0;
     const int nd = 2 * m;
+    HMC_DCHECK(m >= 1 && m <= Tab::kSteps && d0 + nd <= dim && nd <= (int)blockDim.x);
     __syncthreads();  // previous chunk fully consumed
     // lane-part table: thread t owns dimension d0 + t, all 32 Gray codes
     if (threadIdx.x < nd) {
@@ -101,6 +102,7 @@ __device__ __forceinline__ void sobol_refill(Tab& tab, int q0, int m, const Sobo
         const uint32_t sh = a.sobol_scramble ? sobol_shift(sl.key_run, d) : 0u;
         uint32_t* out = reinterpret_cast<uint32_t*>(&tab.U[0][0]) + (dd >> 1) * 2 + (dd & 1);
         for (int r = r0; r < r1; ++r) {
+            HMC_DCHECK(r < Tab::kRows && (dd >> 1) < Tab::kSteps);
             if (r > r0) {
                 B += 32u;
                 const uint32_t g2 = B ^ (B >> 1);
@@ -117,6 +119,7 @@ __device__ __forceinline__ void sobol_refill(Tab& tab, int q0, int m, const Sobo
 // the two left-aligned coordinates X = x << 2 | mid of pair q of the loaded chunk
 template <class Tab>
 __device__ __forceinline__ uint2 sobol_coords(const Tab& tab, int q, const SobolLane& sl) {
+    HMC_DCHECK(q >= 0 && q <= Tab::kSteps && sl.row >= 0 && sl.row < Tab::kRows && sl.jl < 32u);
     const uint2 t = tab.T[q][sl.jl];
     const uint2 u = tab.U[sl.row][q];
     return make_uint2(t.x ^ u.x, t.y ^ u.y);

@@ -60,6 +60,7 @@ __device__ __forceinline__ int strike_bucket(const float* sK, int pow2, int nK, 
 // int conversion is the 1.5*2^23 magic add (FMA pipe, no XU conversion).
 __device__ __forceinline__ void hist_add(int* h, unsigned long long* gdirect, int nb, int v, int c,
                                          float x, float scale) {
+    HMC_DCHECK(v >= 0 && v < kSurfVals && c >= 0 && c < nb);
     const float y = x * scale;
     if (fabsf(y) < 1048576.0f) {
         const int q = __float_as_int(y + 12582912.0f) - 0x4B400000;  // round to nearest
@@ -70,6 +71,7 @@ __device__ __forceinline__ void hist_add(int* h, unsigned long long* gdirect, in
 }
 
 __device__ __forceinline__ void hist_count(int* h, int nb, int v, int c) {
+    HMC_DCHECK(v >= 0 && v < kSurfVals && c >= 0 && c < nb);
     atomicAdd(h + v * nb + c, 1);
 }
 
@@ -77,6 +79,7 @@ __device__ __forceinline__ void hist_count(int* h, int nb, int v, int c) {
 // straddling those strikes; usually zero or one strike)
 __device__ __forceinline__ void band_add(int* h, unsigned long long* g64, int nb, const float* sK,
                                          int row, int lo, int hi, float x) {
+    HMC_DCHECK(lo >= 0 && hi <= nb - 1);
     for (int j = lo; j < hi; ++j) {
         const float e = x - sK[j];
         hist_add(h, g64, nb, row, j, e, kSurfBandScale);
@@ -126,8 +129,10 @@ __device__ __forceinline__ void surface_checkpoint(const PathState32& st, const 
     const int per_style = kSurfVals * nb;
     unsigned long long* g_euro = gacc + ((size_t)0 * s.n_mats + m) * per_style;
     unsigned long long* g_asian = gacc + ((size_t)1 * s.n_mats + m) * per_style;
+    HMC_DCHECK(m >= 0 && m < s.n_mats);
     if (live) {
         const SurfMat mc = s.mats[m];
+        HMC_DCHECK(mc.step >= 1 && mc.step <= a.n_sim);
         const float E = __ldg(a.steps32 + mc.step).x;       // S0 e^{r T_m}
         // European: S_T of each trajectory; r bumps by e^{+-h T}, for which
         // d+ Rp - d- Rm = 0 exactly (the FD numerator is -K (d+ - d-))
@@ -168,6 +173,7 @@ __global__ void __launch_bounds__(kSurfThreads, kSurfMinBlocks) surface_kernel(c
     extern __shared__ int hist[];  // [2][kSurfVals][nK + 1] int32 fixed point
     __shared__ float sK[kSurfMaxStrikes];
     const int nb = s.nK + 1;
+    HMC_DCHECK(s.nK >= 1 && s.nK <= kSurfMaxStrikes && s.n_mats >= 1);
     for (int i = threadIdx.x; i < s.nK; i += blockDim.x) sK[i] = s.strikes[i];
     for (int i = threadIdx.x; i < 2 * kSurfVals * nb; i += blockDim.x) hist[i] = 0;
     __syncthreads();
