@@ -39,6 +39,9 @@
  *                                 gamma_batch and
  *                                 schemes.euler_step / milstein_step
  *                                 (rng.py:63-132, schemes.py:33-61)
+ *   hmc_bessel_f64 / hmc_ivlaw_phi_f64 / hmc_ivlaw_eval_f64 /
+ *   hmc_exact_step_f64         <- bessel.py / ivlaw.py / exact.py: the exact
+ *                                 scheme's host-side spec modules
  *   hmc_root_key / hmc_derive_key
  *                              <- rng.root_key / rng.derive_key (rng.py:46-52)
  *   hmc_philox_check / hmc_box_muller_check / hmc_sobol_quantile_check /
@@ -389,6 +392,38 @@ int hmc_gamma_f64(const uint64_t* keys, const uint64_t* start, int64_t n, double
 int hmc_steps_f64(const hmc_model* model, int32_t milstein, double dt, const double* s,
                   const double* v, const double* u, int64_t n, double* s_out, double* v_out,
                   int32_t device);
+
+/* The reference's exact-scheme host modules, elementwise on the device --
+ * the exact kernel's own routines (hmc_exact.cu, -fmad=false).  All buffers
+ * HOST, synchronous; errors HMC_E_BESSEL / HMC_E_QUAD / HMC_E_ROOT as the
+ * reference raises them.  They serve the drop-in's bessel / ivlaw / exact
+ * modules:
+ *   hmc_bessel_f64     <- bessel.bessel_i_series / bessel_i_series_vec
+ *                         (mode HMC_BESSEL_SERIES), bessel_i (HMC_BESSEL_I),
+ *                         bessel_i_ratio (HMC_BESSEL_RATIO: z = coeff_num,
+ *                         aux[i] = {coeff_den, w, log_coeff_ratio re, im},
+ *                         re = NaN for the principal log) (bessel.py:26-82,
+ *                         _core.pyx:143-159); z, out: [n][2] (re, im)
+ *   hmc_ivlaw_phi_f64  <- ivlaw.characteristic_fn_raw / _characteristic_fn_vec
+ *                         (ivlaw.py:50-108, _core.pyx:162-188): Phi(a[i])
+ *   hmc_ivlaw_eval_f64 <- ivlaw.IntegratedVarianceLaw (ivlaw.py:111-308,
+ *                         _core.pyx:195-310): info = {mean, std, h, nodes}
+ *                         (HMC_IVLAW_INFO, n may be 0), cdf_raw / cdf /
+ *                         inverse_cdf of in[i] (HMC_IVLAW_CDF_RAW / _CDF /
+ *                         _INVERSE)
+ *   hmc_exact_step_f64 <- exact.variance_transition (full = 0) / exact_step
+ *                         (full = 1) (exact.py:38-88): draws[i] = {z1, gamma,
+ *                         u_iv, z3} -> out[i] = {s_t, v_t, integrated var} */
+enum { HMC_BESSEL_SERIES = 0, HMC_BESSEL_I = 1, HMC_BESSEL_RATIO = 2 };
+enum { HMC_IVLAW_INFO = 0, HMC_IVLAW_CDF_RAW = 1, HMC_IVLAW_CDF = 2, HMC_IVLAW_INVERSE = 3 };
+int hmc_bessel_f64(int32_t mode, double nu, const double* z, const double* aux, int64_t n, double* out,
+                   int32_t device);
+int hmc_ivlaw_phi_f64(const hmc_model* model, double v_u, double v_t, double dt, const double* a, int64_t n,
+                      double* out, int32_t device);
+int hmc_ivlaw_eval_f64(const hmc_model* model, double v_u, double v_t, double dt, int32_t mode,
+                       const double* in, int64_t n, double* out, double* info, int32_t device);
+int hmc_exact_step_f64(const hmc_model* model, int32_t full, double s_u, double v_u, double dt,
+                       const double* draws, int64_t n, double* out, int32_t device);
 
 uint64_t hmc_root_key(uint64_t seed);
 uint64_t hmc_derive_key(uint64_t parent, uint64_t index);

@@ -9,15 +9,13 @@ drop-in -- TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 Before collection, ``hestonmc`` and its submodules are aliased to
 ``paper_2309_10477_b200`` (the reference tests import ``hestonmc.engine``,
 ``.model``, ``.errors``, ``.rng``, ``.products``, ``.schemes``,
-``.backend``, ``.cli``).  The reference's two kernel modules are mapped as
+``.backend``, ``.cli``, and the exact scheme's ``.bessel``, ``.ivlaw``,
+``.exact``).  The reference's two kernel modules are mapped as
 the reference's backend seam would see them on this machine:
 ``hestonmc._core`` (the compiled backend) -> the drop-in's GPU backend
 ``cuda_backend``, ``hestonmc._batch_py`` (the other backend of the
 cross-backend tests) -> ``oracle.ref_batch``, the reference's own compiled
-kernel.  Modules the drop-in does not provide (the exact scheme's host
-internals ``bessel``, ``ivlaw``, ``exact.exact_step`` -- SURVEY §2 OUT)
-are left unaliased, so their test modules fail to import and are reported
-as such.
+kernel.
 """
 
 from __future__ import annotations
@@ -32,7 +30,8 @@ if ROOT not in sys.path:
 
 import paper_2309_10477_b200 as _pkg  # noqa: E402
 
-_SUBMODULES = ("engine", "model", "errors", "rng", "products", "schemes", "backend", "cli")
+_SUBMODULES = ("engine", "model", "errors", "rng", "products", "schemes", "backend", "cli", "bessel", "ivlaw",
+               "exact")
 
 sys.modules["hestonmc"] = _pkg
 for _name in _SUBMODULES:

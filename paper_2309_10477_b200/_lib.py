@@ -48,7 +48,10 @@ EXPORTS = (
     "hmc_exact_greeks_chunks", "hmc_slice_chunks", "hmc_comm_unique_id", "hmc_comm_init",
     "hmc_comm_destroy", "hmc_comm_gather_chunks", "hmc_comm_allreduce_sum",
     "hmc_uniforms_f64", "hmc_ndtri_f64", "hmc_steps_f64", "hmc_gamma_f64",
+    "hmc_bessel_f64", "hmc_ivlaw_phi_f64", "hmc_ivlaw_eval_f64", "hmc_exact_step_f64",
 )
+HMC_BESSEL_SERIES, HMC_BESSEL_I, HMC_BESSEL_RATIO = 0, 1, 2
+HMC_IVLAW_INFO, HMC_IVLAW_CDF_RAW, HMC_IVLAW_CDF, HMC_IVLAW_INVERSE = 0, 1, 2, 3
 HMC_COMM_ID_BYTES = 128
 HMC_DTYPE_I64, HMC_DTYPE_F64 = 0, 1
 HMC_SURF_MAX_STRIKES = 128
@@ -141,6 +144,10 @@ def _declare(L: ctypes.CDLL) -> None:
         "hmc_gamma_f64": (ctypes.c_int, [ctypes.POINTER(u64), ctypes.POINTER(u64), i64, dbl, dbl, pd,
                                          ctypes.POINTER(u64), i32]),
         "hmc_steps_f64": (ctypes.c_int, [pM, i32, dbl, pd, pd, pd, i64, pd, pd, i32]),
+        "hmc_bessel_f64": (ctypes.c_int, [i32, dbl, pd, pd, i64, pd, i32]),
+        "hmc_ivlaw_phi_f64": (ctypes.c_int, [pM, dbl, dbl, dbl, pd, i64, pd, i32]),
+        "hmc_ivlaw_eval_f64": (ctypes.c_int, [pM, dbl, dbl, dbl, i32, pd, i64, pd, pd, i32]),
+        "hmc_exact_step_f64": (ctypes.c_int, [pM, i32, dbl, dbl, dbl, pd, i64, pd, i32]),
         "hmc_root_key": (u64, [u64]),
         "hmc_derive_key": (u64, [u64, u64]),
     }

@@ -841,6 +841,109 @@ int hmc_steps_f64(const hmc_model* model, int32_t milstein, double dt, const dou
                             });
 }
 
+// the exact kernel's error codes (_core.pyx:36-40, 508-520) as ABI codes
+static int exact_error(int code) {
+    switch (code) {
+        case 0: return HMC_OK;
+        case 1: return fail(HMC_E_BESSEL, "|z| exceeds the series validity bound 50");
+        case 2: return fail(HMC_E_BESSEL, "Bessel series did not converge");
+        case 3: return fail(HMC_E_QUAD, "characteristic-function tail did not fall below tolerance");
+        default: return fail(HMC_E_ROOT, "CDF inversion failed to reach tolerance");
+    }
+}
+
+int hmc_bessel_f64(int32_t mode, double nu, const double* z, const double* aux, int64_t n, double* out,
+                   int32_t device) {
+    if (mode != HMC_BESSEL_SERIES && mode != HMC_BESSEL_I && mode != HMC_BESSEL_RATIO)
+        return fail(HMC_E_INVALID, "unknown Bessel mode");
+    if (!(nu > -1.0) || !std::isfinite(nu)) return fail(HMC_E_INVALID, "need a finite order nu > -1");
+    if (n < 0 || (n > 0 && (!z || !out || (mode == HMC_BESSEL_RATIO && !aux))))
+        return fail(HMC_E_INVALID, "need z[n][2], out[n][2] (and aux[n][4] for the ratio)");
+    if (n == 0) return HMC_OK;
+    int h_err = 0;
+    const size_t zb = (size_t)n * 16, ab = mode == HMC_BESSEL_RATIO ? (size_t)n * 32 : 0;
+    int rc = elementwise_call(device, {{z, zb}, {aux, ab}}, {{out, zb}, {&h_err, sizeof(int)}},
+                              [&](auto& d, cudaStream_t s) {
+        cudaError_t e = cudaMemsetAsync(d[3], 0, sizeof(int), s);
+        if (e == cudaSuccess)
+            e = hmc::launch_bessel(mode, nu, (const double*)d[0], (const double*)d[1], n, (double*)d[2], (int*)d[3], s);
+        return e;
+    });
+    return rc ? rc : exact_error(h_err);
+}
+
+int hmc_ivlaw_phi_f64(const hmc_model* model, double v_u, double v_t, double dt, const double* a, int64_t n,
+                      double* out, int32_t device) {
+    int rc = check_model(model);
+    if (rc) return rc;
+    if (!(dt > 0.0) || !std::isfinite(dt) || !(v_u >= 0.0) || !(v_t >= 0.0))
+        return fail(HMC_E_INVALID, "need dt > 0 and v_u, v_t >= 0");
+    if (n < 0 || (n > 0 && (!a || !out))) return fail(HMC_E_INVALID, "need a[n] and out[n][2]");
+    if (n == 0) return HMC_OK;
+    int h_err = 0;
+    const double dof = 4.0 * model->kappa * model->theta / (model->sigma * model->sigma);  // model.py:43-45
+    rc = elementwise_call(device, {{a, (size_t)n * 8}}, {{out, (size_t)n * 16}, {&h_err, sizeof(int)}},
+                          [&](auto& d, cudaStream_t s) {
+        cudaError_t e = cudaMemsetAsync(d[2], 0, sizeof(int), s);
+        if (e == cudaSuccess)
+            e = hmc::launch_ivlaw_phi(model->kappa, model->sigma, dof, v_u, v_t, dt, (const double*)d[0], n,
+                                      (double*)d[1], (int*)d[2], s);
+        return e;
+    });
+    return rc ? rc : exact_error(h_err);
+}
+
+int hmc_ivlaw_eval_f64(const hmc_model* model, double v_u, double v_t, double dt, int32_t mode,
+                       const double* in, int64_t n, double* out, double* info, int32_t device) {
+    int rc = check_model(model);
+    if (rc) return rc;
+    if (!(dt > 0.0) || !std::isfinite(dt) || !(v_u >= 0.0) || !(v_t >= 0.0))
+        return fail(HMC_E_INVALID, "need dt > 0 and v_u, v_t >= 0");
+    if (mode < HMC_IVLAW_INFO || mode > HMC_IVLAW_INVERSE) return fail(HMC_E_INVALID, "unknown ivlaw mode");
+    if (n < 0 || (n > 0 && (!in || !out)) || !info) return fail(HMC_E_INVALID, "need in[n], out[n] and info[4]");
+    int h_err = 0;
+    const double dof = 4.0 * model->kappa * model->theta / (model->sigma * model->sigma);
+    const long long threads = n > 0 ? n : 1;
+    rc = elementwise_call(device, {{in, (size_t)n * 8}}, {{out, (size_t)n * 8}, {info, 32}, {&h_err, sizeof(int)}},
+                          [&](auto& d, cudaStream_t s) {
+        double* scratch = nullptr;
+        cudaError_t e = hmc_host::pool_alloc(device, (void**)&scratch,
+                                             (size_t)hmc::kExactCacheNodes * threads * sizeof(double), s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(d[3], 0, sizeof(int), s);
+        if (e == cudaSuccess)
+            e = hmc::launch_ivlaw_eval(mode, model->kappa, model->theta, model->sigma, dof, v_u, v_t, dt,
+                                       (const double*)d[0], n, (double*)d[1], (double*)d[2], scratch, (int*)d[3], s);
+        if (scratch) cudaFreeAsync(scratch, s);
+        return e;
+    });
+    return rc ? rc : exact_error(h_err);
+}
+
+int hmc_exact_step_f64(const hmc_model* model, int32_t full, double s_u, double v_u, double dt,
+                       const double* draws, int64_t n, double* out, int32_t device) {
+    int rc = check_model(model);
+    if (rc) return rc;
+    if (!(dt > 0.0) || !std::isfinite(dt)) return fail(HMC_E_INVALID, "dt must be finite and > 0");
+    if (!(s_u > 0.0) || !(v_u >= 0.0)) return fail(HMC_E_INVALID, "need s_u > 0 and v_u >= 0");
+    if (n < 0 || (n > 0 && (!draws || !out))) return fail(HMC_E_INVALID, "need draws[n][4] and out[n][3]");
+    if (n == 0) return HMC_OK;
+    int h_err = 0;
+    rc = elementwise_call(device, {{draws, (size_t)n * 32}}, {{out, (size_t)n * 24}, {&h_err, sizeof(int)}},
+                          [&](auto& d, cudaStream_t s) {
+        double* scratch = nullptr;
+        cudaError_t e = full ? hmc_host::pool_alloc(device, (void**)&scratch,
+                                                    (size_t)hmc::kExactCacheNodes * n * sizeof(double), s)
+                             : cudaSuccess;
+        if (e == cudaSuccess) e = cudaMemsetAsync(d[2], 0, sizeof(int), s);
+        if (e == cudaSuccess)
+            e = hmc::launch_exact_step(full ? 1 : 0, *model, s_u, v_u, dt, (const double*)d[0], n, (double*)d[1],
+                                       scratch, (int*)d[2], s);
+        if (scratch) cudaFreeAsync(scratch, s);
+        return e;
+    });
+    return rc ? rc : exact_error(h_err);
+}
+
 int hmc_philox_check(const uint32_t* ctr, int32_t n, uint32_t* out, int32_t device) {
     if (!ctr || !out || n < 1) return fail(HMC_E_INVALID, "bad philox check arguments");
     const DeviceGuard keep_device;

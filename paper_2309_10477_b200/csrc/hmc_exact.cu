@@ -20,6 +20,7 @@
 // buffer (node-major, coalesced) and any further node is recomputed on the
 // fly -- identical values, bounded memory.  Typical node counts are 20-130.
 #include <cuda_runtime.h>
+#include <math_constants.h>
 
 #include "hmc_device.cuh"
 #include "hmc_launch.h"
@@ -299,21 +300,32 @@ HMC_EXACT_FN double bisect_iv(double u, double lo, double hi, double h, int n, c
     return 0.0;
 }
 
-// inverse-CDF draw of the conditional integrated variance (_core.pyx:195-310)
-__device__ double sample_iv(double kappa, double theta, double sigma, double dof, double v_u,
-                            double v_t, double dt, double u, NodeCache& nc, int* err) {
+// The law of the conditional integrated variance (ivlaw.py
+// IntegratedVarianceLaw.__post_init__ / _moments, _core.pyx:195-240): the
+// point-mass and degenerate regimes, else the moments from Phi at a small
+// frequency and the quadrature step h; P is the per-path part of Phi.
+enum { kLawQuadrature = 0, kLawPointMass = 1, kLawDegenerate = 2 };
+struct IvLaw {
+    double mean, std, h;
+    int kind;
+};
+
+__device__ __forceinline__ IvLaw iv_law(double kappa, double theta, double sigma, double dof, double v_u,
+                                        double v_t, double dt, PhiPath& P, int* err) {
     const double sigma2 = sigma * sigma;
     const double nu = 0.5 * dof - 1.0;
-    if (u < 1e-12) u = 1e-12;
-    if (u > 1.0 - 1e-12) u = 1.0 - 1e-12;
-    if (sigma < 1e-4 * kappa) return theta * dt + (v_u - theta) * (1.0 - exp(-kappa * dt)) / kappa;
-
+    IvLaw L{0.0, 0.0, 0.0, kLawQuadrature};
+    if (sigma < 1e-4 * kappa) {
+        L.mean = theta * dt + (v_u - theta) * (1.0 - exp(-kappa * dt)) / kappa;
+        L.kind = kLawPointMass;
+        return L;
+    }
     double scale = 0.5 * (v_u + v_t);
     if (scale < 0.01 * theta) scale = 0.01 * theta;
     scale *= dt;
     double m1 = scale, eps;
     cplx phi;
-    const PhiPath P = phi_path(kappa, sigma2, nu, v_u, v_t, dt);
+    P = phi_path(kappa, sigma2, nu, v_u, v_t, dt);
     for (int it = 0; it < 2; ++it) {
         eps = 0.05 / m1;
         phi = phi_node(P, eps, err);
@@ -327,13 +339,56 @@ __device__ double sample_iv(double kappa, double theta, double sigma, double dof
     const double m2 = -2.0 * (phi.re - 1.0) / (eps * eps);
     double var = m2 - m1 * m1;
     if (var < 0.0) var = 0.0;
-    const double mean = m1, std = sqrt(var);
+    L.mean = m1;
+    L.std = sqrt(var);
+    if (L.std < kDegenerateRelStd * L.mean) L.kind = kLawDegenerate;
+    L.h = 2.0 * kPi / (L.mean + kPeriodStds * L.std);
+    return L;
+}
+
+// Re Phi at the quadrature nodes j h, j = 1.., into the cache until the tail
+// criterion holds (_core.pyx: (2/pi) |Phi(j h)| / j below tolerance for
+// kTailRun nodes in a row); on_node(j, Re Phi) sees every node.  Returns
+// the node count (0 with *err set past kMaxNodes).
+template <class OnNode>
+__device__ __forceinline__ int iv_nodes(const PhiPath& P, double h, const NodeCache& nc, OnNode on_node,
+                                        int* err) {
+    int n = 0, run = 0;
+    while (run < kTailRun) {
+        if (n >= kMaxNodes) {
+            *err = kErrQuad;
+            return 0;
+        }
+        const int j = n + 1;
+        const cplx p = phi_node(P, j * h, err);
+        if (*err != kErrNone) return 0;
+        if (n < nc.cap) nc.base[(size_t)n * nc.stride] = p.re;
+        on_node(j, p.re);
+        // (2/pi) |p| / j < tol, compared squared
+        const double tj = kTailTol * j;
+        if ((4.0 / (kPi * kPi)) * norm2_(p) < tj * tj)
+            ++run;
+        else
+            run = 0;
+        ++n;
+    }
+    return n;
+}
+
+// inverse-CDF draw of the conditional integrated variance (_core.pyx:195-310)
+__device__ double sample_iv(double kappa, double theta, double sigma, double dof, double v_u,
+                            double v_t, double dt, double u, NodeCache& nc, int* err) {
+    if (u < 1e-12) u = 1e-12;
+    if (u > 1.0 - 1e-12) u = 1.0 - 1e-12;
+    PhiPath P;
+    const IvLaw L = iv_law(kappa, theta, sigma, dof, v_u, v_t, dt, P, err);
+    if (L.kind == kLawPointMass) return L.mean;
     if (*err != kErrNone) return 0.0;
-    if (std < kDegenerateRelStd * mean) {
-        const double r = mean + std * ndtri_ref(u);
+    if (L.kind == kLawDegenerate) {
+        const double r = L.mean + L.std * ndtri_ref(u);
         return r > 0.0 ? r : 0.0;
     }
-    const double h = 2.0 * kPi / (mean + kPeriodStds * std);
+    const double h = L.h, mean = L.mean;
     nc.P = &P;
     nc.h = h;
 
@@ -344,26 +399,8 @@ __device__ double sample_iv(double kappa, double theta, double sigma, double dof
     if (x < 1e-3 * hi) x = 1e-3 * hi;
     if (x > 0.9 * hi) x = 0.9 * hi;
     NewtonSums first(h, x);
-
-    int n = 0, run = 0;
-    while (run < kTailRun) {
-        if (n >= kMaxNodes) {
-            *err = kErrQuad;
-            return 0.0;
-        }
-        const int j = n + 1;
-        const cplx p = phi_node(P, j * h, err);
-        if (*err != kErrNone) return 0.0;
-        if (n < nc.cap) nc.base[(size_t)n * nc.stride] = p.re;
-        first.add(j, p.re);
-        // (2/pi) |p| / j < tol, compared squared
-        const double tj = kTailTol * j;
-        if ((4.0 / (kPi * kPi)) * norm2_(p) < tj * tj)
-            ++run;
-        else
-            run = 0;
-        ++n;
-    }
+    const int n = iv_nodes(P, h, nc, [&](int j, double re) { first.add(j, re); }, err);
+    if (*err != kErrNone) return 0.0;
 
     for (int it = 0; it < kNewtonMaxIter; ++it) {
         NewtonSums ns = first;
@@ -614,6 +651,180 @@ __global__ void gamma_kernel(const unsigned long long* __restrict__ keys,
 cudaError_t launch_gamma(const unsigned long long* d_keys, const unsigned long long* d_start, long long n,
                          double shape, double scale, double* d_out, unsigned long long* d_used, cudaStream_t s) {
     gamma_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(d_keys, d_start, n, shape, scale, d_out, d_used);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// The reference's exact-scheme host modules (bessel.py, ivlaw.py, exact.py)
+// as elementwise kernels over the exact kernel's own device routines: the
+// Bessel series, the characteristic function, the law's moments, nodes,
+// CDF and Newton inversion, and one exact step on given draws.  One thread
+// per input; the law's nodes live in a per-thread scratch slice like the
+// batch kernel's.  Errors: the batch kernel's codes, max over threads.
+// ---------------------------------------------------------------------------
+namespace {
+__device__ __forceinline__ cplx clog_(cplx a) { return {log(cabs_(a)), atan2(a.im, a.re)}; }
+}  // namespace
+
+// bessel.py: mode 0 bessel_i_series, 1 bessel_i, 2 bessel_i_ratio (z =
+// coeff_num; aux[4 i ..] = coeff_den, w, log_coeff_ratio re / im, re NaN for
+// the principal log of coeff_num / coeff_den)
+__global__ void bessel_kernel(int mode, double nu, const double* __restrict__ z, const double* __restrict__ aux,
+                              long long n, double* __restrict__ out, int* err) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int e = kErrNone;
+    const cplx zz = cx(z[2 * i], z[2 * i + 1]);
+    cplx r;
+    if (mode == HMC_BESSEL_SERIES) {
+        r = bessel_series(nu, zz, &e);
+    } else if (mode == HMC_BESSEL_I) {
+        const cplx ser = bessel_series(nu, zz, &e);
+        if (zz.re == 0.0 && zz.im == 0.0)   // the limits at z = 0 (bessel.py bessel_i)
+            r = nu > 0.0 ? cx(0.0) : (nu == 0.0 ? ser / exp(lgamma(nu + 1.0)) : cx(CUDART_INF));
+        else
+            r = cexp_(nu * clog_(0.5 * zz) - cx(lgamma(nu + 1.0))) * ser;
+    } else {
+        const double cd = aux[4 * i], w = aux[4 * i + 1];
+        const cplx s_num = bessel_series(nu, w * zz, &e);
+        const cplx s_den = bessel_series(nu, cx(w * cd), &e);
+        const cplx lr = isnan(aux[4 * i + 2]) ? clog_(zz / cd) : cx(aux[4 * i + 2], aux[4 * i + 3]);
+        r = (cexp_(nu * lr) * s_num) / s_den;
+    }
+    out[2 * i] = r.re;
+    out[2 * i + 1] = r.im;
+    if (e != kErrNone) atomicMax(err, e);
+}
+
+cudaError_t launch_bessel(int mode, double nu, const double* d_z, const double* d_aux, long long n, double* d_out,
+                          int* d_err, cudaStream_t s) {
+    bessel_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(mode, nu, d_z, d_aux, n, d_out, d_err);
+    return cudaGetLastError();
+}
+
+// ivlaw.py characteristic_fn_raw / _characteristic_fn_vec: Phi(a) at each a
+__global__ void ivlaw_phi_kernel(double kappa, double sigma, double dof, double v_u, double v_t, double dt,
+                                 const double* __restrict__ a, long long n, double* __restrict__ out, int* err) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int e = kErrNone;
+    cplx p = cx(1.0);
+    if (a[i] != 0.0) {   // Phi(0) = 1 exactly, no series evaluated
+        const PhiPath P = phi_path(kappa, sigma * sigma, 0.5 * dof - 1.0, v_u, v_t, dt);
+        p = phi_node(P, a[i], &e);
+    }
+    out[2 * i] = p.re;
+    out[2 * i + 1] = p.im;
+    if (e != kErrNone) atomicMax(err, e);
+}
+
+cudaError_t launch_ivlaw_phi(double kappa, double sigma, double dof, double v_u, double v_t, double dt,
+                             const double* d_a, long long n, double* d_out, int* d_err, cudaStream_t s) {
+    ivlaw_phi_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(kappa, sigma, dof, v_u, v_t, dt, d_a, n, d_out,
+                                                                 d_err);
+    return cudaGetLastError();
+}
+
+// ivlaw.py IntegratedVarianceLaw: info[0..3] = mean, std, h, node count
+// (thread 0), and per input (mode) cdf_raw(x), cdf(x) or inverse_cdf(u)
+__global__ void ivlaw_eval_kernel(int mode, double kappa, double theta, double sigma, double dof, double v_u,
+                                  double v_t, double dt, const double* __restrict__ in, long long n,
+                                  double* __restrict__ out, double* __restrict__ info, double* scratch,
+                                  long long stride, int* err) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (n > 0 ? n : 1)) return;
+    int e = kErrNone;
+    NodeCache nc{};
+    nc.base = scratch + i;
+    nc.stride = stride;
+    nc.cap = kExactCacheNodes;
+    PhiPath P;
+    const IvLaw L = iv_law(kappa, theta, sigma, dof, v_u, v_t, dt, P, &e);
+    const bool degenerate = L.kind != kLawQuadrature && L.std < kDegenerateRelStd * L.mean;
+    // nodes: for cdf_raw always (the reference evaluates its quadrature even
+    // in a degenerate regime), for cdf only outside the degenerate regimes,
+    // for the info of a quadrature law (the converged node count)
+    const bool want_nodes = e == kErrNone && L.kind != kLawPointMass &&
+                            (mode == HMC_IVLAW_CDF_RAW || (mode == HMC_IVLAW_CDF && L.kind == kLawQuadrature) ||
+                             (mode == HMC_IVLAW_INFO && L.kind == kLawQuadrature));
+    int n_nodes = 0;
+    if (want_nodes) {
+        nc.P = &P;
+        nc.h = L.h;
+        n_nodes = iv_nodes(P, L.h, nc, [](int, double) {}, &e);
+    }
+    if (i == 0) {
+        info[0] = L.mean;
+        info[1] = L.std;
+        info[2] = L.h;
+        info[3] = (double)n_nodes;
+    }
+    if (n > 0 && e == kErrNone) {
+        const double x = in[i];
+        double r = 0.0;
+        if (mode == HMC_IVLAW_INVERSE) {
+            r = sample_iv(kappa, theta, sigma, dof, v_u, v_t, dt, x, nc, &e);
+        } else if (mode == HMC_IVLAW_CDF && (L.kind == kLawPointMass || degenerate || L.kind == kLawDegenerate)) {
+            if (L.std == 0.0)
+                r = x < L.mean ? 0.0 : 1.0;
+            else
+                r = x > 0.0 ? 0.5 * erfc(-((x - L.mean) / L.std) / sqrt(2.0)) : 0.0;
+        } else if (x > 0.0) {
+            r = cdf_at(x, L.h, n_nodes, nc, &e);
+            if (mode == HMC_IVLAW_CDF) r = fmin(fmax(r, 0.0), 1.0);
+        }
+        out[i] = r;
+    }
+    if (e != kErrNone) atomicMax(err, e);
+}
+
+cudaError_t launch_ivlaw_eval(int mode, double kappa, double theta, double sigma, double dof, double v_u,
+                              double v_t, double dt, const double* d_in, long long n, double* d_out, double* d_info,
+                              double* d_scratch, int* d_err, cudaStream_t s) {
+    const long long threads = n > 0 ? n : 1;
+    ivlaw_eval_kernel<<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(
+        mode, kappa, theta, sigma, dof, v_u, v_t, dt, d_in, n, d_out, d_info, d_scratch, threads, d_err);
+    return cudaGetLastError();
+}
+
+// exact.py variance_transition (full = 0) / exact_step (full = 1) on given
+// draws [z1, gamma, u_iv, z3] per row: the batch kernel's step arithmetic
+__global__ void exact_step_kernel(int full, hmc_model m, double dof, double s_u, double v_u, double dt,
+                                  const double* __restrict__ draws, long long n, double* __restrict__ out,
+                                  double* scratch, int* err) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int e = kErrNone;
+    const double* d = draws + 4 * i;
+    const double ek = exp(-m.kappa * dt);
+    const double c = m.sigma * m.sigma * (1.0 - ek) / (4.0 * m.kappa);
+    const double lam = 4.0 * m.kappa * ek * v_u / (m.sigma * m.sigma * (1.0 - ek));
+    const double shifted = d[0] + sqrt(lam);
+    const double v_t = c * (d[1] + shifted * shifted);
+    double s_t = s_u, iv = 0.0;
+    if (full) {
+        NodeCache nc{};
+        nc.base = scratch + i;
+        nc.stride = n;
+        nc.cap = kExactCacheNodes;
+        iv = sample_iv(m.kappa, m.theta, m.sigma, dof, v_u, v_t, dt, d[2], nc, &e);
+        const double int_w2 = m.sigma < 1e-4 * m.kappa ? sqrt(iv) * ndtri_ref(d[2])
+                                                       : (v_t - v_u - m.kappa * m.theta * dt + m.kappa * iv) / m.sigma;
+        double var_ln = (1.0 - m.rho * m.rho) * iv;
+        if (var_ln < 0.0) var_ln = 0.0;
+        s_t = exp(log(s_u) + m.r * dt - 0.5 * iv + m.rho * int_w2 + sqrt(var_ln) * d[3]);
+    }
+    out[3 * i] = s_t;
+    out[3 * i + 1] = v_t;
+    out[3 * i + 2] = iv;
+    if (e != kErrNone) atomicMax(err, e);
+}
+
+cudaError_t launch_exact_step(int full, const hmc_model& m, double s_u, double v_u, double dt, const double* d_draws,
+                              long long n, double* d_out, double* d_scratch, int* d_err, cudaStream_t s) {
+    const double dof = 4.0 * m.kappa * m.theta / (m.sigma * m.sigma);  // model.py:43-45
+    exact_step_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(full, m, dof, s_u, v_u, dt, d_draws, n, d_out,
+                                                                  d_scratch, d_err);
     return cudaGetLastError();
 }
 

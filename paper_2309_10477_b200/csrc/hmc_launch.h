@@ -115,6 +115,16 @@ cudaError_t launch_uniforms(const unsigned long long* d_keys, long long n_keys,
                             const unsigned long long* d_draws, long long n, double* d_out, cudaStream_t s);
 cudaError_t launch_ndtri(const double* d_u, long long n, double* d_out, cudaStream_t s);
 // Marsaglia-Tsang Gamma on the reference stream (hmc_exact.cu)
+// the reference's exact-scheme host modules on the device (hmc_exact.cu)
+cudaError_t launch_bessel(int mode, double nu, const double* d_z, const double* d_aux, long long n, double* d_out,
+                          int* d_err, cudaStream_t s);
+cudaError_t launch_ivlaw_phi(double kappa, double sigma, double dof, double v_u, double v_t, double dt,
+                             const double* d_a, long long n, double* d_out, int* d_err, cudaStream_t s);
+cudaError_t launch_ivlaw_eval(int mode, double kappa, double theta, double sigma, double dof, double v_u,
+                              double v_t, double dt, const double* d_in, long long n, double* d_out, double* d_info,
+                              double* d_scratch, int* d_err, cudaStream_t s);
+cudaError_t launch_exact_step(int full, const hmc_model& m, double s_u, double v_u, double dt, const double* d_draws,
+                              long long n, double* d_out, double* d_scratch, int* d_err, cudaStream_t s);
 cudaError_t launch_gamma(const unsigned long long* d_keys, const unsigned long long* d_start, long long n,
                          double shape, double scale, double* d_out, unsigned long long* d_used, cudaStream_t s);
 cudaError_t launch_steps(const KernelArgs& a, const double* d_s, const double* d_v, const double* d_u,

@@ -16,21 +16,89 @@ shares the chunk exchange across GPUs and the fixed-shape run reduction
 engine's 4096-path job sums + ``math.fsum`` to ~1e-15 relative (the
 summation order differs; the golden tests hold them to 1e-12).
 
-Greeks beyond the reference's pathwise Delta/Rho: the S0 bump (and the r
-bump of a European) is an exact rescaling of the simulated path (ln S
-starts at ln S0 and accumulates r dt); the v0 bumps and the Asian r bumps
-re-run the exact kernel on the same streams (common random numbers) -- the
-reference's own finite-difference method (tests/test_products.py:101-137).
+Greeks beyond the reference's pathwise Delta/Rho: the S0 and r bumps are
+exact rescalings of the simulated path (ln S starts at ln S0 and accumulates
+r dt, so S_k(r +- h) = S_k e^{+-h t_k}); the v0 bumps re-run the exact
+kernel on the same streams (common random numbers) -- the reference's own
+finite-difference method (tests/test_products.py:101-137).
+
+The module also carries the reference's scalar exact-step API
+(``hestonmc/exact.py``: ``nccs_coefficients``, ``variance_transition``,
+``ExactStepResult``, ``exact_step``), drawing from the caller's streams in
+the reference's order and evaluating the step on the device with the exact
+kernel's arithmetic (``hmc_exact_step_f64``).
 """
 
 from __future__ import annotations
 
 import ctypes
+import math
+from dataclasses import dataclass
 
 import numpy as np
 
-from . import _lib, parallel, sobol
+from . import _lib, parallel, rng, sobol
+from .errors import InvalidParams
 from .model import HestonParams, OptionSpec, SimConfig
+
+
+# ---- the reference's scalar exact step (exact.py) ----------------------------
+
+def nccs_coefficients(params: HestonParams, dt: float, v_u: float) -> tuple[float, float]:
+    """(scale c, noncentrality lambda) of v_t = c chi'2_d(lambda) (exact.py:22-33)."""
+    if dt <= 0.0:
+        raise InvalidParams(f"dt must be > 0, got {dt}")
+    kappa, sigma = params.kappa, params.sigma
+    ek = math.exp(-kappa * dt)
+    return (sigma * sigma * (1.0 - ek) / (4.0 * kappa),
+            4.0 * kappa * ek * v_u / (sigma * sigma * (1.0 - ek)))
+
+
+def _device_step(params: HestonParams, full: bool, s_u: float, v_u: float, dt: float,
+                 draws: list[float]) -> np.ndarray:
+    d = np.ascontiguousarray(draws, dtype=np.float64)
+    out = np.empty(3)
+    dp = ctypes.POINTER(ctypes.c_double)
+    m = _lib.Model(params.kappa, params.theta, params.sigma, params.rho, params.r, params.v0)
+    _lib.check(_lib.lib().hmc_exact_step_f64(ctypes.byref(m), int(full), float(s_u), float(v_u), float(dt),
+                                             d.ctypes.data_as(dp), 1, out.ctypes.data_as(dp), rng._device()))
+    return out
+
+
+def variance_transition(stream, params: HestonParams, v_u: float, dt: float, gamma_stream=None) -> float:
+    """v_t given v_u from the scaled non-central chi-squared law: one normal
+    from ``stream``, the Gamma part from ``gamma_stream`` (default ``stream``)."""
+    _, lam = nccs_coefficients(params, dt, v_u)
+    p = rng.NccsParams(dof=params.dof, noncentrality=lam)
+    z = rng.sample_normal(stream)
+    g = rng.sample_gamma(gamma_stream if gamma_stream is not None else stream, 0.5 * (p.dof - 1.0), 2.0)
+    return float(_device_step(params, False, 1.0, v_u, dt, [z, g, 0.5, 0.0])[1])
+
+
+@dataclass(frozen=True)
+class ExactStepResult:
+    s_t: float
+    v_t: float
+    integrated_variance: float
+
+
+def exact_step(stream, params: HestonParams, s_u: float, v_u: float, dt: float,
+               gamma_stream=None) -> ExactStepResult:
+    """One exact transition of (S, V) over [u, u + dt]: variance transition,
+    integrated variance by CDF inversion, int sqrt(V) dW2 from the endpoints,
+    Gaussian ln S_t -- three logical draws from ``stream`` in the reference's
+    order (normal, inversion uniform, normal), the Gamma from its substream."""
+    if s_u <= 0.0:
+        raise InvalidParams(f"s_u must be > 0, got {s_u}")
+    _, lam = nccs_coefficients(params, dt, v_u)
+    p = rng.NccsParams(dof=params.dof, noncentrality=lam)
+    z1 = rng.sample_normal(stream)
+    g = rng.sample_gamma(gamma_stream if gamma_stream is not None else stream, 0.5 * (p.dof - 1.0), 2.0)
+    u_iv = stream.next_uniform()
+    z3 = rng.sample_normal(stream)
+    s_t, v_t, iv = _device_step(params, True, s_u, v_u, dt, [z1, g, u_iv, z3])
+    return ExactStepResult(s_t=float(s_t), v_t=float(v_t), integrated_variance=float(iv))
+
 
 
 def exact_step_times(spec: OptionSpec) -> np.ndarray:

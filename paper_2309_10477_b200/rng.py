@@ -155,9 +155,9 @@ class UniformStream:
     dimension: int = 1
     stream_index: int = 0
     _key: int = field(init=False, default=0)
-    _counter: int = field(init=False, default=0)
+    _fetched: int = field(init=False, default=0, repr=False)   # draws (pseudo) / points (sobol) fetched
     _buffer: np.ndarray | None = field(init=False, default=None, repr=False)
-    _buf_pos: int = field(init=False, default=0)
+    _buf_pos: int = field(init=False, default=0, repr=False)
 
     _CHUNK = 4096
 
@@ -170,13 +170,20 @@ class UniformStream:
             raise ValidationError("stream_index must be >= 0")
         self._key = stream_key(self.seed, self.stream_index)
 
+    @property
+    def _counter(self) -> int:
+        """The reference's counter (rng.py:171-207): draws consumed so far
+        for a pseudo stream (its draws are fetched from the device in
+        blocks, consumed one at a time), points fetched for a sobol one."""
+        return self._position() if self.kind == "pseudo" else self._fetched
+
     def _refill(self):
         if self.kind == "pseudo":
-            self._buffer = uniforms_at(self._key, self._counter, self._CHUNK)
+            self._buffer = uniforms_at(self._key, self._fetched, self._CHUNK)
         else:
-            start = 1 + self.stream_index * SOBOL_BLOCK + self._counter
+            start = 1 + self.stream_index * SOBOL_BLOCK + self._fetched
             self._buffer = sobol_points(self.dimension, start, self._CHUNK).reshape(-1)
-        self._counter += self._CHUNK
+        self._fetched += self._CHUNK
         self._buf_pos = 0
 
     def next_uniform(self) -> float:
@@ -190,12 +197,12 @@ class UniformStream:
     def _position(self) -> int:
         """Index of the next draw (pseudo streams)."""
         pending = 0 if self._buffer is None else self._buffer.size - self._buf_pos
-        return self._counter - pending
+        return self._fetched - pending
 
     def _skip(self, n: int) -> None:
         """Consume n draws (pseudo streams)."""
         pos = self._position() + n
-        self._buffer, self._buf_pos, self._counter = None, 0, pos
+        self._buffer, self._buf_pos, self._fetched = None, 0, pos
 
     def next_point(self) -> np.ndarray:
         return np.array([self.next_uniform() for _ in range(self.dimension)])

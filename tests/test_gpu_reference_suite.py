@@ -3,13 +3,13 @@
 ``make -C oracle`` copies ``/root/reference/pkg/tests`` into the git-ignored
 ``oracle/_ref/tests`` (it travels to the GPU box like the reference kernel
 build); ``oracle/refsuite_shim.py`` aliases ``hestonmc`` to the package
-before collection.  Every test of the in-scope modules (engine, products,
+before collection.  Every test of the modules (engine, products,
 acceptance, backends, cli, schemes, rng) runs; the outcome must match the
 ledger below exactly: every test not listed passes, and each listed test
 fails for the stated design reason (DESIGN.md §7 carries the same list).
-The exact scheme's host internals (``test_bessel``, ``test_ivlaw``,
-``test_exact``: Bessel series, integrated-variance law, scalar exact step --
-SURVEY §2 OUT) are not provided by the drop-in and are not collected.
+Since round 2 that includes the exact scheme's host modules (``test_bessel``,
+``test_ivlaw``, ``test_exact``: Bessel series, integrated-variance law,
+scalar exact step), served by the exact kernel's device routines.
 """
 
 import json
@@ -23,7 +23,8 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SUITE = os.path.join(ROOT, "oracle", "_ref", "tests")
 MODULES = ("test_engine.py", "test_products.py", "test_acceptance.py", "test_backends.py",
-           "test_cli.py", "test_schemes.py", "test_rng.py")
+           "test_cli.py", "test_schemes.py", "test_rng.py", "test_bessel.py", "test_ivlaw.py",
+           "test_exact.py")
 
 pytestmark = pytest.mark.gpu
 
@@ -40,8 +41,6 @@ EXPECTED_FAILURES = {
         "profiles/r02_se_scaling_seed_sweep.txt: 5 % for the fp32 Philox stream AND for the "
         "reference's own stream); at seed 42 the fp32 stream's ratio is 0.785 (bound 0.65); the "
         "same test on the reference's stream (precision='fp64', the replay path) gives 0.559 and passes",
-    "test_acceptance.py::test_criterion_7_property_suite":
-        "imports hestonmc.ivlaw (the exact scheme's host integrated-variance law, SURVEY §2 OUT)",
 }
 
 

@@ -88,5 +88,18 @@ for spec in (OptionSpec("european", "call", 100.0, 1.0, 100.0),
             finite([v.estimate for v in greeks(p, spec, cfg).values()], "exact greeks")
 finite(cuda_backend.exact_batch(p, 100.0, np.array([0.0, 0.5, 1.0]), np.array([1, 1]), 3, 2000, 11, None),
        "exact_batch")
+# the exact scheme's host modules (bessel / ivlaw / exact step) on the device
+from paper_2309_10477_b200 import bessel, exact, ivlaw, rng
+finite([abs(bessel.bessel_i(nu, z)) for nu in (-0.37, 0.0, 1.5) for z in (0.5 + 1j, 20.0 + 0j, 45 - 3j)], "bessel_i")
+finite(np.abs(bessel.bessel_i_series_vec(-0.37, np.array([0.1 + 0j, 3 - 2j, 40 + 10j]))), "bessel series")
+finite(abs(bessel.bessel_i_ratio(-0.37, 2 + 1.5j, 2.4, 0.8)), "bessel ratio")
+for v_u, v_t, dt in ((0.010201, 0.010201, 1.0), (0.04, 0.01, 0.25), (0.0, 0.02, 1.0 / 252)):
+    law = ivlaw.IntegratedVarianceLaw(p, v_u, v_t, dt)
+    finite([law.mean, law.std, law.cdf(law.mean), law.cdf_raw(0.5 * law.mean), law.inverse_cdf(0.3)], "ivlaw")
+    finite(np.abs(ivlaw._characteristic_fn_vec(p, v_u, v_t, dt, np.array([0.0, 0.3, 30.0, 3000.0]))), "phi")
+st = rng.UniformStream(seed=4)
+res = exact.exact_step(st, p, 100.0, 0.010201, 1.0, gamma_stream=rng.UniformStream(seed=4, stream_index=1))
+finite([res.s_t, res.v_t, res.integrated_variance], "exact_step")
+finite(exact.variance_transition(rng.UniformStream(seed=5), p, 0.02, 0.5), "variance_transition")
 print("exact ok", flush=True)
 print(f"checked suite ok ({n_calls} checked calls)")
