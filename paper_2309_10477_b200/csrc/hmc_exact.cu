@@ -740,13 +740,13 @@ __global__ void ivlaw_eval_kernel(int mode, double kappa, double theta, double s
     nc.cap = kExactCacheNodes;
     PhiPath P;
     const IvLaw L = iv_law(kappa, theta, sigma, dof, v_u, v_t, dt, P, &e);
-    const bool degenerate = L.kind != kLawQuadrature && L.std < kDegenerateRelStd * L.mean;
+    const bool degenerate = L.std < kDegenerateRelStd * L.mean;   // ivlaw.py is_degenerate
     // nodes: for cdf_raw always (the reference evaluates its quadrature even
-    // in a degenerate regime), for cdf only outside the degenerate regimes,
-    // for the info of a quadrature law (the converged node count)
+    // in a degenerate regime), for cdf and the info (the converged node
+    // count) outside the degenerate regimes
     const bool want_nodes = e == kErrNone && L.kind != kLawPointMass &&
-                            (mode == HMC_IVLAW_CDF_RAW || (mode == HMC_IVLAW_CDF && L.kind == kLawQuadrature) ||
-                             (mode == HMC_IVLAW_INFO && L.kind == kLawQuadrature));
+                            (mode == HMC_IVLAW_CDF_RAW || ((mode == HMC_IVLAW_CDF || mode == HMC_IVLAW_INFO) &&
+                                                           !degenerate));
     int n_nodes = 0;
     if (want_nodes) {
         nc.P = &P;
@@ -764,7 +764,7 @@ __global__ void ivlaw_eval_kernel(int mode, double kappa, double theta, double s
         double r = 0.0;
         if (mode == HMC_IVLAW_INVERSE) {
             r = sample_iv(kappa, theta, sigma, dof, v_u, v_t, dt, x, nc, &e);
-        } else if (mode == HMC_IVLAW_CDF && (L.kind == kLawPointMass || degenerate || L.kind == kLawDegenerate)) {
+        } else if (mode == HMC_IVLAW_CDF && degenerate) {
             if (L.std == 0.0)
                 r = x < L.mean ? 0.0 : 1.0;
             else

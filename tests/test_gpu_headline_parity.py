@@ -7,6 +7,8 @@ its per-path statistics and its CRN finite-difference method, seed 42).
   combined standard errors of the reference's 2^24-path statistics, whose SE
   is no larger than the GPU's (same path count) -- the north star's target.
 * C2 -- European call, 2^22 x 252 full Greeks (the bench's secondary job).
+* C4 -- randomised Sobol QMC (time-ordered and bridge-ordered) on the C3
+  job, 16 shifts x 2^22 points, against the same C3 statistics.
 * C5 -- the bench's surface job (64 strikes x 8 maturities, European + daily
   Asian, 2^22 paths x 504 steps): 20 (strike, maturity, style) points --
   deep ITM, ATM, deep OTM, short and long maturities, both styles -- each
@@ -59,6 +61,29 @@ def test_c2_european_full_greeks_within_3se():
     ref = load_json("stats_c2_2p22.json")["euro"]
     zs = {q: _z(g[q].estimate, g[q].path_std_error, ref[q]) for q in QN}
     assert all(abs(z) <= 3.0 for z in zs.values()), zs
+
+
+@pytest.mark.parametrize("bridge", [0, 16])
+def test_c4_rqmc_sobol_vs_reference_statistics(bridge):
+    """C4 -- randomised Sobol QMC (time-ordered and Brownian-bridge ordered),
+    the bench's Asian job at 16 digital shifts x 2^22 points: all seven
+    quantities within 3 combined SE of the reference's 2^24-path C3
+    statistics (the QMC SE is the run-to-run SD / sqrt(16): the points of
+    one run are not independent, so the per-path SE does not apply)."""
+    import dataclasses
+    sys.path.insert(0, ROOT)
+    import bench
+    p, spec, cfg = bench.workload()
+    R = 16
+    cfg = dataclasses.replace(cfg, sampler="sobol", sobol_highdim_ack=True, sobol_scramble=True,
+                              sobol_bridge=bridge, n_paths=2**22, n_runs=R)
+    g = greeks(p, spec, cfg)
+    ref = load_json("stats_c3_2p24.json")["asian_daily"]
+    zs = {q: _z(g[q].estimate, g[q].std_error / math.sqrt(R), ref[q]) for q in QN}
+    assert all(abs(z) <= 3.0 for z in zs.values()), zs
+    # and QMC pays: the price's run-to-run SE is well below the pseudo-random
+    # per-path SE at the same total path count (2^26)
+    assert g["price"].std_error / math.sqrt(R) < 0.5 * ref["price"][1] / 2.0
 
 
 def test_c5_surface_points_vs_reference_crn():

@@ -6,7 +6,7 @@ build); ``oracle/refsuite_shim.py`` aliases ``hestonmc`` to the package
 before collection.  Every test of the modules (engine, products,
 acceptance, backends, cli, schemes, rng) runs; the outcome must match the
 ledger below exactly: every test not listed passes, and each listed test
-fails for the stated design reason (DESIGN.md §7 carries the same list).
+fails for the stated design reason (INTEGRATION.md §4 carries the same list).
 Since round 2 that includes the exact scheme's host modules (``test_bessel``,
 ``test_ivlaw``, ``test_exact``: Bessel series, integrated-variance law,
 scalar exact step), served by the exact kernel's device routines.
