@@ -86,13 +86,20 @@ def secondary_workloads(reps: int = 3, sm_mhz: float = 1965.0, max_over_ranks=No
     ranks; path-steps/s is whole-job."""
     import numpy as np
     import torch
-    from paper_2309_10477_b200 import (BENCH_PARAMS, HestonParams, OptionSpec, SimConfig, greeks,
+    from paper_2309_10477_b200 import (BENCH_PARAMS, HestonParams, OptionSpec, SimConfig, engine, greeks,
                                        price, surface, daily_fixings)
     p = HestonParams(**BENCH_PARAMS)
     euro = OptionSpec("european", "call", 100.0, 1.0, 100.0)
     asian = OptionSpec("asian_arithmetic", "call", 100.0, 1.0, 100.0,
                        averaging_times=daily_fixings(1.0, N_STEPS))
     jobs = {
+        # config 1 (the reference's CPU-runnable case): European price + Delta,
+        # 1e5 paths x 252 Milstein steps, the reference's greeks() keys --
+        # launch- and latency-bound at this size
+        "c1_european_price_delta_1e5x252": (
+            lambda: engine._execute(p, euro, SimConfig(scheme="milstein", n_paths=100_000, n_steps=252,
+                                                       n_runs=1, seed=7), want_greeks=False),
+            100_000 * 252),
         "c2_european_full_greeks_2^22x252": (
             lambda: greeks(p, euro, SimConfig(scheme="milstein", n_paths=2**22, n_steps=252,
                                               n_runs=1, seed=7)), 2**22 * 252),

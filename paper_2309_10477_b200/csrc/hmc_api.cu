@@ -904,15 +904,23 @@ int hmc_ivlaw_eval_f64(const hmc_model* model, double v_u, double v_t, double dt
     int h_err = 0;
     const double dof = 4.0 * model->kappa * model->theta / (model->sigma * model->sigma);
     const long long threads = n > 0 ? n : 1;
+    // node-cache scratch: kExactCacheNodes doubles per thread, so inputs go in
+    // batches of at most kBatch (~128 MB of scratch)
+    constexpr long long kBatch = 1LL << 16;
+    const long long batch = std::min(threads, kBatch);
     rc = elementwise_call(device, {{in, (size_t)n * 8}}, {{out, (size_t)n * 8}, {info, 32}, {&h_err, sizeof(int)}},
                           [&](auto& d, cudaStream_t s) {
         double* scratch = nullptr;
         cudaError_t e = hmc_host::pool_alloc(device, (void**)&scratch,
-                                             (size_t)hmc::kExactCacheNodes * threads * sizeof(double), s);
+                                             (size_t)hmc::kExactCacheNodes * batch * sizeof(double), s);
         if (e == cudaSuccess) e = cudaMemsetAsync(d[3], 0, sizeof(int), s);
-        if (e == cudaSuccess)
+        for (long long off = 0; e == cudaSuccess && (off < n || (n == 0 && off == 0)); off += batch) {
+            const long long m = n == 0 ? 0 : std::min(batch, n - off);
             e = hmc::launch_ivlaw_eval(mode, model->kappa, model->theta, model->sigma, dof, v_u, v_t, dt,
-                                       (const double*)d[0], n, (double*)d[1], (double*)d[2], scratch, (int*)d[3], s);
+                                       (const double*)d[0] + off, m, (double*)d[1] + off, (double*)d[2], scratch,
+                                       (int*)d[3], s);
+            if (n == 0) break;
+        }
         if (scratch) cudaFreeAsync(scratch, s);
         return e;
     });
@@ -928,16 +936,18 @@ int hmc_exact_step_f64(const hmc_model* model, int32_t full, double s_u, double 
     if (n < 0 || (n > 0 && (!draws || !out))) return fail(HMC_E_INVALID, "need draws[n][4] and out[n][3]");
     if (n == 0) return HMC_OK;
     int h_err = 0;
+    constexpr long long kBatch = 1LL << 16;   // node-cache scratch per batch (as hmc_ivlaw_eval_f64)
+    const long long batch = std::min((long long)n, kBatch);
     rc = elementwise_call(device, {{draws, (size_t)n * 32}}, {{out, (size_t)n * 24}, {&h_err, sizeof(int)}},
                           [&](auto& d, cudaStream_t s) {
         double* scratch = nullptr;
         cudaError_t e = full ? hmc_host::pool_alloc(device, (void**)&scratch,
-                                                    (size_t)hmc::kExactCacheNodes * n * sizeof(double), s)
+                                                    (size_t)hmc::kExactCacheNodes * batch * sizeof(double), s)
                              : cudaSuccess;
         if (e == cudaSuccess) e = cudaMemsetAsync(d[2], 0, sizeof(int), s);
-        if (e == cudaSuccess)
-            e = hmc::launch_exact_step(full ? 1 : 0, *model, s_u, v_u, dt, (const double*)d[0], n, (double*)d[1],
-                                       scratch, (int*)d[2], s);
+        for (long long off = 0; e == cudaSuccess && off < n; off += batch)
+            e = hmc::launch_exact_step(full ? 1 : 0, *model, s_u, v_u, dt, (const double*)d[0] + 4 * off,
+                                       std::min(batch, n - off), (double*)d[1] + 3 * off, scratch, (int*)d[2], s);
         if (scratch) cudaFreeAsync(scratch, s);
         return e;
     });
