@@ -97,15 +97,20 @@ enum { kErrNone = 0, kErrBesselRange = 1, kErrBesselConv = 2, kErrQuad = 3, kErr
 
 // power series of the modified Bessel function I_nu(z) / ((z/2)^nu / Gamma(nu+1))
 // (_core.pyx:143-159)
-HMC_EXACT_FN cplx bessel_series(double nu, cplx z, int* err) {
+// inv_kn: optional table of 1 / (k (nu + k)), k = 1..kBesselTerms, for the
+// kernels whose nu is fixed per launch (the same IEEE quotient the division
+// computes -- bit-identical -- but a shared-memory load instead of a fp64
+// reciprocal per term)
+constexpr int kBesselTerms = 400;
+HMC_EXACT_FN cplx bessel_series(double nu, cplx z, int* err, const double* inv_kn = nullptr) {
     if (cabs_(z) > 50.0) {
         *err = kErrBesselRange;
         return cx(0.0);
     }
     const cplx q = 0.25 * (z * z);
     cplx term = cx(1.0), total = cx(1.0);
-    for (int k = 1; k <= 400; ++k) {
-        term = term * q / (k * (nu + k));
+    for (int k = 1; k <= kBesselTerms; ++k) {
+        term = inv_kn ? inv_kn[k - 1] * (term * q) : term * q / (k * (nu + k));
         total = total + term;
         // |term| < 1e-12 |total|, compared squared (no square roots)
         if (norm2_(term) < 1e-24 * norm2_(total)) return total;
@@ -125,10 +130,13 @@ struct PhiPath {
     double ek, one_m_ek, kb, vs, w, log1m_ek, ekh_inv;  // ekh_inv = e^{kappa tau / 2}
     cplx den;      // bessel_series(nu, w coeff_k)
     int den_err;   // its error code (kErrNone = 0)
+    const double* inv_kn;  // bessel_series' optional 1 / (k (nu + k)) table
 };
 
-HMC_EXACT_FN PhiPath phi_path(double kappa, double sigma2, double nu, double v_u, double v_t, double tau) {
+HMC_EXACT_FN PhiPath phi_path(double kappa, double sigma2, double nu, double v_u, double v_t, double tau,
+                              const double* inv_kn = nullptr) {
     PhiPath P;
+    P.inv_kn = inv_kn;
     P.kappa = kappa;
     P.sigma2 = sigma2;
     P.nu = nu;
@@ -143,7 +151,7 @@ HMC_EXACT_FN PhiPath phi_path(double kappa, double sigma2, double nu, double v_u
     P.w = sqrt(v_u * v_t);
     P.log1m_ek = log(1.0 - P.ek);
     P.den_err = 0;
-    P.den = bessel_series(nu, cx(P.w * coeff_k), &P.den_err);
+    P.den = bessel_series(nu, cx(P.w * coeff_k), &P.den_err, inv_kn);
     return P;
 }
 
@@ -168,14 +176,18 @@ HMC_EXACT_FN cplx phi_node(const PhiPath& P, double a, int* err) {
     const cplx bracket = cx(P.kb) - (g * (one + eg)) * inv_ome;
     const cplx coeff_g = (4.0 / sigma2) * ge;
     // log q = log(g / kappa) - (g - kappa) tau / 2 + log(1 - e^{-kappa tau}) - log(1 - e^{-g tau}),
-    // the two real logarithms merged into one (the arguments keep their own
-    // atan2 branches, exactly as the two complex logarithms)
+    // the two real logarithms merged into one, and the two arguments too:
+    // Re g > 0 (principal root), so |e^{-g tau}| < 1 and Re(1 - e^{-g tau}) > 0
+    // -- both principal arguments lie in (-pi/2, pi/2), their difference in
+    // (-pi, pi), so arg(g/kappa) - arg(ome) = arg(g/kappa conj(ome)) exactly
+    // (one atan2 instead of two: they were ~11 % of the kernel's samples)
     const cplx gk = g / kappa;
     const cplx half_gt = 0.5 * ((g - cx(kappa)) * cx(tau));
+    const cplx gko = gk * cx(ome.re, -ome.im);
     const cplx log_q = {0.5 * log(norm2_(gk) / norm2_(ome)) - half_gt.re + P.log1m_ek,
-                        atan2(gk.im, gk.re) - half_gt.im - atan2(ome.im, ome.re)};
+                        atan2(gko.im, gko.re) - half_gt.im};
     const cplx expo = cexp_(P.vs * bracket + nu * log_q);   // e^{vs bracket} q^nu
-    const cplx ser = bessel_series(nu, P.w * coeff_g, err);
+    const cplx ser = bessel_series(nu, P.w * coeff_g, err, P.inv_kn);
     if (P.den_err != kErrNone) *err = P.den_err;
     return lead * expo * (ser / P.den.re);   // the denominator series has a real argument: real
 }
@@ -311,7 +323,8 @@ struct IvLaw {
 };
 
 __device__ __forceinline__ IvLaw iv_law(double kappa, double theta, double sigma, double dof, double v_u,
-                                        double v_t, double dt, PhiPath& P, int* err) {
+                                        double v_t, double dt, PhiPath& P, int* err,
+                                        const double* inv_kn = nullptr) {
     const double sigma2 = sigma * sigma;
     const double nu = 0.5 * dof - 1.0;
     IvLaw L{0.0, 0.0, 0.0, kLawQuadrature};
@@ -325,7 +338,7 @@ __device__ __forceinline__ IvLaw iv_law(double kappa, double theta, double sigma
     scale *= dt;
     double m1 = scale, eps;
     cplx phi;
-    P = phi_path(kappa, sigma2, nu, v_u, v_t, dt);
+    P = phi_path(kappa, sigma2, nu, v_u, v_t, dt, inv_kn);
     for (int it = 0; it < 2; ++it) {
         eps = 0.05 / m1;
         phi = phi_node(P, eps, err);
@@ -377,11 +390,12 @@ __device__ __forceinline__ int iv_nodes(const PhiPath& P, double h, const NodeCa
 
 // inverse-CDF draw of the conditional integrated variance (_core.pyx:195-310)
 __device__ double sample_iv(double kappa, double theta, double sigma, double dof, double v_u,
-                            double v_t, double dt, double u, NodeCache& nc, int* err) {
+                            double v_t, double dt, double u, NodeCache& nc, int* err,
+                            const double* inv_kn = nullptr) {
     if (u < 1e-12) u = 1e-12;
     if (u > 1.0 - 1e-12) u = 1.0 - 1e-12;
     PhiPath P;
-    const IvLaw L = iv_law(kappa, theta, sigma, dof, v_u, v_t, dt, P, err);
+    const IvLaw L = iv_law(kappa, theta, sigma, dof, v_u, v_t, dt, P, err, inv_kn);
     if (L.kind == kLawPointMass) return L.mean;
     if (*err != kErrNone) return 0.0;
     if (L.kind == kLawDegenerate) {
@@ -457,6 +471,13 @@ __global__ void __launch_bounds__(kExactThreads, MINB) exact_batch_kernel(const 
     const long long n = e.path_hi - e.path_lo;
     const long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long stride = (long long)gridDim.x * blockDim.x;
+    // the Bessel series' 1 / (k (nu + k)) for this launch's nu, once per block
+    __shared__ double inv_kn[kBesselTerms];
+    {
+        const double nu = 0.5 * e.dof - 1.0;
+        for (int k = threadIdx.x + 1; k <= kBesselTerms; k += blockDim.x) inv_kn[k - 1] = 1.0 / (k * (nu + k));
+        __syncthreads();
+    }
     NodeCache nc{};
     nc.base = e.scratch + slot;
     nc.stride = stride;
@@ -513,7 +534,7 @@ __global__ void __launch_bounds__(kExactThreads, MINB) exact_batch_kernel(const 
             const double g = sample_gamma(derive(gamma_root, (unsigned long long)k), 0.5 * (e.dof - 1.0), 2.0);
             const double shifted = z1 + sqrt(lam);
             const double v_new = c * (g + shifted * shifted);
-            const double iv = sample_iv(e.kappa, e.theta, e.sigma, e.dof, v, v_new, dt, u2, nc, &err);
+            const double iv = sample_iv(e.kappa, e.theta, e.sigma, e.dof, v, v_new, dt, u2, nc, &err, inv_kn);
             if (err != kErrNone) break;
             double int_w2;
             if (point_mass)
