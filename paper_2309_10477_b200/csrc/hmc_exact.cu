@@ -131,6 +131,12 @@ struct PhiPath {
     cplx den;      // bessel_series(nu, w coeff_k)
     int den_err;   // its error code (kErrNone = 0)
     const double* inv_kn;  // bessel_series' optional 1 / (k (nu + k)) table
+    // per-path quotients of phi_node, hoisted (the same IEEE operations on
+    // the same inputs: bit-identical to evaluating them at every node)
+    double inv_kappa;   // 1 / kappa                  (g / kappa)
+    double lead_c;      // e^{kappa tau/2} (1 - e^{-kappa tau}) / kappa
+    double four_s2;     // 4 / sigma^2
+    double inv_den;     // 1 / den.re                 (ser / den.re)
 };
 
 HMC_EXACT_FN PhiPath phi_path(double kappa, double sigma2, double nu, double v_u, double v_t, double tau,
@@ -152,6 +158,10 @@ HMC_EXACT_FN PhiPath phi_path(double kappa, double sigma2, double nu, double v_u
     P.log1m_ek = log(1.0 - P.ek);
     P.den_err = 0;
     P.den = bessel_series(nu, cx(P.w * coeff_k), &P.den_err, inv_kn);
+    P.inv_kappa = 1.0 / kappa;
+    P.lead_c = P.ekh_inv * P.one_m_ek / kappa;
+    P.four_s2 = 4.0 / sigma2;
+    P.inv_den = 1.0 / P.den.re;
     return P;
 }
 
@@ -172,16 +182,16 @@ HMC_EXACT_FN cplx phi_node(const PhiPath& P, double a, int* err) {
     const cplx ome = one - eg;
     const cplx inv_ome = one / ome;
     const cplx ge = (g * egh) * inv_ome;
-    const cplx lead = (P.ekh_inv * P.one_m_ek / kappa) * ge;
+    const cplx lead = P.lead_c * ge;
     const cplx bracket = cx(P.kb) - (g * (one + eg)) * inv_ome;
-    const cplx coeff_g = (4.0 / sigma2) * ge;
+    const cplx coeff_g = P.four_s2 * ge;
     // log q = log(g / kappa) - (g - kappa) tau / 2 + log(1 - e^{-kappa tau}) - log(1 - e^{-g tau}),
     // the two real logarithms merged into one, and the two arguments too:
     // Re g > 0 (principal root), so |e^{-g tau}| < 1 and Re(1 - e^{-g tau}) > 0
     // -- both principal arguments lie in (-pi/2, pi/2), their difference in
     // (-pi, pi), so arg(g/kappa) - arg(ome) = arg(g/kappa conj(ome)) exactly
     // (one atan2 instead of two: they were ~11 % of the kernel's samples)
-    const cplx gk = g / kappa;
+    const cplx gk = {g.re * P.inv_kappa, g.im * P.inv_kappa};   // g / kappa (operator/ is r = 1/s, then a r)
     const cplx half_gt = 0.5 * ((g - cx(kappa)) * cx(tau));
     const cplx gko = gk * cx(ome.re, -ome.im);
     const cplx log_q = {0.5 * log(norm2_(gk) / norm2_(ome)) - half_gt.re + P.log1m_ek,
@@ -189,7 +199,8 @@ HMC_EXACT_FN cplx phi_node(const PhiPath& P, double a, int* err) {
     const cplx expo = cexp_(P.vs * bracket + nu * log_q);   // e^{vs bracket} q^nu
     const cplx ser = bessel_series(nu, P.w * coeff_g, err, P.inv_kn);
     if (P.den_err != kErrNone) *err = P.den_err;
-    return lead * expo * (ser / P.den.re);   // the denominator series has a real argument: real
+    // the denominator series has a real argument: real (ser / den.re, as r = 1/s then ser r)
+    return lead * expo * cx(ser.re * P.inv_den, ser.im * P.inv_den);
 }
 
 // Marsaglia-Tsang on the reference stream (_core.pyx:116-136), from draw
