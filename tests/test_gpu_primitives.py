@@ -20,6 +20,7 @@ import pytest
 
 from conftest import load_json
 from paper_2309_10477_b200 import rng, schemes
+from paper_2309_10477_b200.errors import BesselNonConvergence, InvalidParams
 from paper_2309_10477_b200.model import GridSpec, HestonParams, BENCH_PARAMS
 
 pytestmark = pytest.mark.gpu
@@ -109,3 +110,56 @@ def test_simulate_path_equals_backend_on_same_draws(scheme):
     for _ in range(32):
         state = step(st, p, state, grid.dt)
     assert math.isclose(state.s, obs.s_T, rel_tol=1e-14)
+
+
+# ---------------------------------------------------------------------------
+# The exact scheme's host modules on the device (bessel / ivlaw / exact):
+# the same routines the exact kernel runs (csrc/hmc_exact.cu), checked here
+# against scipy and against the exact kernel itself.  The reference's own
+# test_bessel / test_ivlaw / test_exact modules also run unmodified in
+# tests/test_gpu_reference_suite.py.
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("nu", [-0.3658, 0.0, 1.5])
+def test_bessel_i_matches_scipy(nu):
+    from scipy.special import iv
+    from paper_2309_10477_b200 import bessel
+    for z in (0.05, 1.0, 7.5, 30.0, 49.0):
+        ours = bessel.bessel_i(nu, complex(z, 0.0))
+        assert abs(ours.imag) <= 1e-10 * abs(iv(nu, z))
+        assert _rel(ours.real, float(iv(nu, z))) <= 1e-10
+    with pytest.raises(BesselNonConvergence):
+        bessel.bessel_i_series(nu, 50.5 + 0j)
+    vec = bessel.bessel_i_series_vec(nu, np.array([0.1 + 0.2j, 3 - 4j, 20 + 1j]))
+    for z, v in zip((0.1 + 0.2j, 3 - 4j, 20 + 1j), vec):
+        assert v == bessel.bessel_i_series(nu, z)
+
+
+def test_ivlaw_round_trip_and_exact_kernel_draw():
+    """inverse_cdf(u) satisfies |F(x) - u| < 1e-6, and it is the value the
+    exact kernel draws for the same (v_u, v_t, dt, u): one exact step on
+    given draws (hmc_exact_step_f64) reports the same integrated variance."""
+    from paper_2309_10477_b200 import exact, ivlaw
+    p = HestonParams(**BENCH_PARAMS)
+    law = ivlaw.IntegratedVarianceLaw(p, 0.04, 0.03, 0.25)
+    assert law.mean > 0.0 and law.std > 0.0 and not law.is_degenerate
+    for u in (1e-6, 0.02, 0.5, 0.98, 1 - 1e-6):
+        x = law.inverse_cdf(u)
+        assert abs(law.cdf_raw(x) - u) < 1e-6
+    # the step's v_t is c (g + (z1 + sqrt(lambda))^2); choose draws giving v_t = 0.03
+    c, lam = exact.nccs_coefficients(p, 0.25, 0.04)
+    g = 0.03 / c - (0.3 + math.sqrt(lam)) ** 2
+    out = exact._device_step(p, True, 100.0, 0.04, 0.25, [0.3, g, 0.37, -0.2])
+    assert _rel(out[1], 0.03) <= 1e-14
+    law2 = ivlaw.IntegratedVarianceLaw(p, 0.04, out[1], 0.25)
+    assert _rel(out[2], law2.inverse_cdf(0.37)) <= 1e-14
+
+
+def test_exact_step_draw_budget():
+    from paper_2309_10477_b200 import exact
+    p = HestonParams(**BENCH_PARAMS)
+    main, gam = rng.UniformStream(seed=5), rng.UniformStream(seed=5, stream_index=1)
+    res = exact.exact_step(main, p, 100.0, 0.04, 0.5, gamma_stream=gam)
+    assert main._counter == 3 and gam._counter > 0
+    assert res.s_t > 0.0 and res.v_t >= 0.0 and res.integrated_variance > 0.0
+    with pytest.raises(InvalidParams):
+        exact.exact_step(rng.UniformStream(seed=5), p, 0.0, 0.04, 0.5)
