@@ -47,3 +47,29 @@ def test_repeated_calls_are_bit_identical_and_leak_free():
     free1 = torch.cuda.mem_get_info()[0]
     assert torch.cuda.memory_allocated() == alloc0
     assert free0 - free1 < 64 * 2**20, (free0, free1)   # nothing accumulates on the device
+
+
+def test_missing_extension_fails_loudly_on_a_gpu_box(tmp_path):
+    """With a GPU visible but libhmc.so missing, every entry point raises
+    DeviceError -- there is no CPU path to fall back to."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, numpy as np\n"
+        f"sys.path.insert(0, {root!r})\n"
+        "from paper_2309_10477_b200 import DeviceError, HestonParams, OptionSpec, SimConfig, greeks, cuda_backend\n"
+        "p = HestonParams(2.0, 0.04, 0.3, -0.7, 0.03, 0.04)\n"
+        "spec = OptionSpec('european', 'call', 100.0, 1.0, 100.0)\n"
+        "n = 0\n"
+        "for f in (lambda: greeks(p, spec, SimConfig(scheme='milstein', n_paths=1024, n_steps=8, n_runs=1)),\n"
+        "          lambda: cuda_backend.discretised_batch(p, 100.0, 1.0, 8, True, 0, 16, 1, None, np.array([8]))):\n"
+        "    try:\n"
+        "        f()\n"
+        "    except DeviceError:\n"
+        "        n += 1\n"
+        "print('raised', n)\n")
+    env = dict(os.environ, HMC_LIB_PATH=str(tmp_path / "no_such_libhmc.so"))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "raised 2" in r.stdout, (r.stdout, r.stderr[-2000:])
